@@ -1,0 +1,134 @@
+/*
+ * stencilpipe_b200.h -- C ABI of the B200-native Jacobi hot path.
+ *
+ * The reference (`stencilpipe`, pure Python/numpy) has no FFI; its seam is the
+ * Python function layer listed per entry point below.  This library replaces
+ * the arithmetic under that seam; the Python package paper_0912_4506_b200
+ * binds it with ctypes and keeps the reference's API above it.
+ * (R = /root/reference/pkg/src/stencilpipe)
+ *
+ * Conventions
+ *  - Plain C types only.  Device buffers are allocated by the caller (PyTorch)
+ *    and passed as raw pointers to the START of the allocation; the library
+ *    never allocates or frees grid memory.  Streams are cudaStream_t passed as
+ *    void* (0 = legacy default stream).
+ *  - Every entry point returns 0 (SP_OK) or an SP_ERR_* code; sp_last_error()
+ *    returns a thread-local message for the last failure on that thread.
+ *  - Grid layout: C order (z, y, x), x contiguous; ghost depths gx/gy/gz are
+ *    present on both sides; interior element (z,y,x) lives at
+ *    base[origin + z*pz + y*py + x].  TMA needs py*sizeof(elem) % 16 == 0 and a
+ *    16-byte-aligned base; sp_layout_make() returns such a layout (interior row
+ *    start 128-byte aligned).
+ */
+#ifndef STENCILPIPE_B200_H
+#define STENCILPIPE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SP_OK 0
+#define SP_ERR_GRID 1         /* -> GridError(ValueError)          R/grid.py:25      */
+#define SP_ERR_SCHEDULE 2     /* -> ScheduleError(ValueError)      R/pipeline.py:30  */
+#define SP_ERR_DECOMP 3       /* -> DecompositionError(ValueError) R/decomp.py:26    */
+#define SP_ERR_DEVICE 4       /* -> RuntimeError (CUDA failure)                      */
+#define SP_ERR_ARG 5          /* -> ValueError (bad argument)                        */
+
+#define SP_F64 0
+#define SP_F32 1
+
+typedef struct sp_layout {
+    int64_t nx, ny, nz;       /* interior extents (GridDims, R/grid.py:29-51)    */
+    int64_t gx, gy, gz;       /* ghost depth present in memory on each side      */
+    int64_t py, pz;           /* row / plane pitch, elements                     */
+    int64_t origin;           /* element offset of interior (0,0,0) from base    */
+} sp_layout;
+
+/* Initial-value pattern, evaluated over GLOBAL coordinates (FillPattern,
+ * R/grid.py:66-118; subdomain shift as _ShiftedPattern, R/decomp.py:107-117).
+ * kind: 0 constant, 1 linear, 2 hotplate, 3 random(seed), 4 2*random-1.
+ * has_faces: cells outside the global interior [0, gn) take faces[] of the
+ * first face beyond which they lie, in the order (z-, z+, y-, y+, x-, x+). */
+typedef struct sp_pattern {
+    int32_t kind;
+    int32_t has_faces;
+    double value;
+    uint64_t seed;
+    int64_t gorigin[3];       /* global (z,y,x) of the local interior origin */
+    int64_t gn[3];            /* global interior extents (z,y,x)             */
+    double faces[6];
+} sp_pattern;
+
+/* Library identity / diagnostics. */
+int sp_version(void);
+const char* sp_last_error(void);
+/* Number of device kernels this library has launched since load. */
+uint64_t sp_launch_count(void);
+
+/* Padded device layout for a grid (replaces the dense numpy allocation of
+ * TwoGrid, R/grid.py:126-134).  *alloc_elems = elements to allocate. */
+int sp_layout_make(int64_t nx, int64_t ny, int64_t nz, int64_t gx, int64_t gy,
+                   int64_t gz, int dtype, sp_layout* out, int64_t* alloc_elems);
+
+/* K3: fill every cell of the allocation from the pattern (ghost shell
+ * included; row padding set to 0).  Replaces FillPattern.evaluate over the
+ * ghosted box in TwoGrid.__init__ (R/grid.py:96-134). */
+int sp_fill(void* base, int dtype, const sp_layout* L, const sp_pattern* p,
+            void* stream);
+
+/* K1: one Jacobi level over the logical box [lo, hi) (z,y,x), dst = stencil(src)
+ * there, every other dst cell untouched.  Replaces update_region
+ * (R/kernel.py:37-40) and hence sweep_naive / sweep_spatial_blocked /
+ * update_block (R/kernel.py:43-80,124-147).  The box may reach into the ghost
+ * shell up to depth-1 (R/kernel.py:138-140). */
+int sp_update_region(const void* src, void* dst, int dtype, const sp_layout* L,
+                     const int64_t lo[3], const int64_t hi[3], void* stream);
+
+/* K2: T levels in one pass over HBM (temporally blocked wavefront), reading
+ * src (level 0) and writing level T into dst over [lo, hi) only.  Level t
+ * (1..T) updates the domain [lo - ext_lo*(T-t), hi + ext_hi*(T-t)) per axis
+ * and keeps every other cell at its previous-level value, so ext = 0 gives
+ * Dirichlet walls and ext = 1 the shrinking extended domains of a rank face
+ * with a neighbour (level_domains_for_rank, R/decomp.py:192-205).  Equivalent
+ * to T node-sweep levels of run_node_sweeps (R/pipeline.py:395-408,459-462).
+ * 1 <= T <= 8. */
+int sp_sweep_tb(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+                const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+                const int32_t ext_hi[3], void* stream);
+
+/* K2 restricted to an output sub-box: identical level domains (lo, hi, ext_*)
+ * as sp_sweep_tb, but only cells of [out_lo, out_hi) (a subset of [lo, hi))
+ * are computed to level T and written.  Used to run a rank's boundary slabs
+ * first and its interior while the halo exchange is in flight
+ * (outer_step + exchange_halos, R/decomp.py:149-237, with overlap added). */
+int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+                     const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+                     const int32_t ext_hi[3], const int64_t out_lo[3],
+                     const int64_t out_hi[3], void* stream);
+
+/* `levels` full-interior sweeps as passes of depth T (last pass shorter),
+ * ping-ponging a/b.  *active: in = which array holds the current level
+ * (0 = a), out = which holds the result (TwoGrid.active, R/grid.py:136-149).
+ * Replaces `levels` calls of sweep_naive (R/kernel.py:43-47). */
+int sp_run_sweeps(void* a, void* b, int dtype, const sp_layout* L, int64_t levels,
+                  int T, int* active, void* stream);
+
+/* K5: order-independent 64-bit digest of the interior (definition in
+ * oracle/jacobi_oracle.c).  Synchronises the stream. */
+int sp_digest(const void* base, int dtype, const sp_layout* L, uint64_t* out,
+              void* stream);
+
+/* Measured FP64 add throughput of this device (DADD/s over all SMs) -- the
+ * compute roof of the stencil, which has no fusable multiply-add. */
+int sp_probe_fp64(double* dadd_per_s, double* ms);
+
+/* Tuning hook: number of resident CTAs per SM the scheduler assumes (0 =
+ * auto) and z-chunk override (0 = auto).  Returns the previous values. */
+int sp_set_tuning(int ctas_per_sm, int chunks);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,149 @@
+"""ctypes binding of libstencilpipe_b200.so (include/stencilpipe_b200.h).
+
+The library is built in-tree (``build()`` / ``__graft_entry__.build()``) and
+loaded from this package directory.  There is no CPU fallback: if the library
+is missing or no CUDA device is visible, calls raise ``NativeUnavailable``.
+Error codes map to the reference's exception types:
+GridError, ScheduleError, DecompositionError (all ValueError) and
+RuntimeError for device failures.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import sys
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_HERE)
+LIB_NAME = "libstencilpipe_b200.so"
+LIB_PATH = os.path.join(_HERE, LIB_NAME)
+SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "jacobi_kernels.cuh")]
+HEADER = os.path.join(_ROOT, "include", "stencilpipe_b200.h")
+
+SP_OK, SP_ERR_GRID, SP_ERR_SCHEDULE, SP_ERR_DECOMP, SP_ERR_DEVICE, SP_ERR_ARG = range(6)
+SP_F64, SP_F32 = 0, 1
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "--shared", "-Xcompiler", "-fPIC",
+    "-Xptxas", "-v",
+]
+
+# Symbols include/stencilpipe_b200.h declares (checked by the CPU tests).
+EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "sp_fill",
+           "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_run_sweeps",
+           "sp_digest", "sp_probe_fp64", "sp_set_tuning")
+
+
+class NativeUnavailable(RuntimeError):
+    """The CUDA library is not built or no B200 is visible."""
+
+
+class Layout(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in
+                ("nx", "ny", "nz", "gx", "gy", "gz", "py", "pz", "origin")]
+
+    def as_tuple(self):
+        return tuple(getattr(self, f) for f, _ in self._fields_)
+
+
+class Pattern(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("has_faces", ctypes.c_int32),
+                ("value", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("gorigin", ctypes.c_int64 * 3), ("gn", ctypes.c_int64 * 3),
+                ("faces", ctypes.c_double * 6)]
+
+
+def build(verbose: bool = False, force: bool = False) -> str:
+    """Compile the sm_100a library in-tree with nvcc; returns its path."""
+    newest = max(os.path.getmtime(p) for p in SOURCES + [HEADER])
+    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
+        return LIB_PATH
+    nvcc = os.environ.get("NVCC", "nvcc")
+    if not any(os.access(os.path.join(p, "nvcc"), os.X_OK)
+               for p in os.environ.get("PATH", "").split(os.pathsep)):
+        if os.path.exists("/usr/local/cuda/bin/nvcc"):
+            nvcc = "/usr/local/cuda/bin/nvcc"
+    tmp = LIB_PATH + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, "-o", tmp, os.path.join(_HERE, "csrc", "capi.cu")]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nvcc failed:\n{res.stderr}")
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(tmp, LIB_PATH)
+    with open(os.path.join(_HERE, "csrc", "ptxas.log"), "w") as fh:
+        fh.write(res.stderr)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def load_library():
+    """Load (not initialise CUDA) -- usable on CPU-only hosts for symbol checks."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailable(f"{LIB_PATH} is not built; run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    P = ctypes.POINTER
+    vp = ctypes.c_void_p
+    i64p = P(ctypes.c_int64)
+    i32p = P(ctypes.c_int32)
+    L.sp_version.restype = ctypes.c_int
+    L.sp_last_error.restype = ctypes.c_char_p
+    L.sp_launch_count.restype = ctypes.c_uint64
+    L.sp_layout_make.argtypes = [ctypes.c_int64] * 6 + [ctypes.c_int, P(Layout), i64p]
+    L.sp_fill.argtypes = [vp, ctypes.c_int, P(Layout), P(Pattern), vp]
+    L.sp_update_region.argtypes = [vp, vp, ctypes.c_int, P(Layout), i64p, i64p, vp]
+    L.sp_sweep_tb.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int, i64p, i64p,
+                              i32p, i32p, vp]
+    L.sp_sweep_tb_part.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int, i64p, i64p,
+                                   i32p, i32p, i64p, i64p, vp]
+    L.sp_run_sweeps.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int64, ctypes.c_int,
+                                P(ctypes.c_int), vp]
+    L.sp_digest.argtypes = [vp, ctypes.c_int, P(Layout), P(ctypes.c_uint64), vp]
+    L.sp_probe_fp64.argtypes = [P(ctypes.c_double), P(ctypes.c_double)]
+    L.sp_set_tuning.argtypes = [ctypes.c_int, ctypes.c_int]
+    for name in EXPORTS:
+        getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
+    _lib = L
+    return L
+
+
+def lib():
+    """The library, after checking a CUDA device is present (no fallback)."""
+    L = load_library()
+    import torch
+    if not torch.cuda.is_available():
+        raise NativeUnavailable("no CUDA device visible: the Jacobi engine has no CPU path")
+    return L
+
+
+def check(rc: int) -> None:
+    if rc == SP_OK:
+        return
+    msg = (load_library().sp_last_error() or b"").decode()
+    from .grid import GridError
+    from .pipeline import ScheduleError
+    from .decomp import DecompositionError
+    exc = {SP_ERR_GRID: GridError, SP_ERR_SCHEDULE: ScheduleError,
+           SP_ERR_DECOMP: DecompositionError, SP_ERR_ARG: ValueError}.get(rc, RuntimeError)
+    raise exc(msg)
+
+
+def i64x3(v):
+    return (ctypes.c_int64 * 3)(*[int(x) for x in v])
+
+
+def i32x3(v):
+    return (ctypes.c_int32 * 3)(*[int(x) for x in v])
+
+
+def launch_count() -> int:
+    return int(load_library().sp_launch_count())

@@ -1,0 +1,372 @@
+// capi.cu -- extern "C" boundary of libstencilpipe_b200.so (include/stencilpipe_b200.h).
+//
+// Host-side work scheduling for the kernels in jacobi_kernels.cuh: layout
+// policy, TMA descriptor encoding, tile/z-chunk partitioning sized to the SM
+// count, argument validation and error reporting.  No grid memory is owned
+// here; the Python layer (PyTorch) allocates and passes raw pointers.
+#include "jacobi_kernels.cuh"
+#include "../../include/stencilpipe_b200.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <mutex>
+#include <string>
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+int g_ctas_per_sm = 0;
+int g_chunks = 0;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+    return fail(SP_ERR_DEVICE, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+#define SP_CUDA(expr)                                   \
+    do {                                                \
+        cudaError_t _e = (expr);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+    } while (0)
+
+int elem_size(int dtype) { return dtype == SP_F64 ? 8 : (dtype == SP_F32 ? 4 : 0); }
+
+int64_t lo_x_mod(int64_t v, int64_t m) { return ((v % m) + m) % m; }
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+struct DevInfo {
+    int sms = 0;
+    int max_smem = 0;
+};
+
+int dev_info(DevInfo* d) {
+    int dev = 0;
+    SP_CUDA(cudaGetDevice(&dev));
+    SP_CUDA(cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, dev));
+    SP_CUDA(cudaDeviceGetAttribute(&d->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    return SP_OK;
+}
+
+int check_layout(const sp_layout* L, int dtype) {
+    if (!L) return fail(SP_ERR_ARG, "null layout");
+    if (elem_size(dtype) == 0) return fail(SP_ERR_ARG, "unknown dtype %d", dtype);
+    if (L->nx < 1 || L->ny < 1 || L->nz < 1)
+        return fail(SP_ERR_GRID, "interior extents must be >= 1, got (%lld, %lld, %lld)",
+                    (long long)L->nx, (long long)L->ny, (long long)L->nz);
+    if (L->gx < 1 || L->gy < 1 || L->gz < 1) return fail(SP_ERR_GRID, "ghost depth must be >= 1");
+    int64_t x_off = L->origin - L->gz * L->pz - L->gy * L->py;
+    if (x_off < L->gx || x_off + L->nx + L->gx > L->py || L->py * (L->ny + 2 * L->gy) > L->pz)
+        return fail(SP_ERR_GRID, "inconsistent layout pitches");
+    if ((L->py * elem_size(dtype)) % 16 != 0)
+        return fail(SP_ERR_GRID, "row pitch must be a multiple of 16 bytes for TMA");
+    if (L->nz + 2 * L->gz >= (1ll << 31) || L->ny + 2 * L->gy >= (1ll << 31) || L->py >= (1ll << 31))
+        return fail(SP_ERR_GRID, "extent exceeds 2^31");
+    return SP_OK;
+}
+
+template <typename R, int T>
+int launch_tb_t(const void* src, void* dst, const sp_layout* L, const sp::TBArgs& a, int grid,
+                cudaStream_t stream) {
+    constexpr int PLANE = sp::WX * sp::WY;
+    constexpr int NLVL = (T > 1) ? (T - 1) : 1;
+    const size_t smem = (size_t)(sp::RING + NLVL) * PLANE * sizeof(R) + sp::RING * sizeof(uint64_t);
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        SP_CUDA(cudaFuncSetAttribute(sp::tb_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+        attr_set = true;
+    }
+    auto enc = encode_fn();
+    if (!enc) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+    CUtensorMap map;
+    const int64_t x_off = L->origin - L->gz * L->pz - L->gy * L->py;
+    cuuint64_t gdim[3] = {(cuuint64_t)L->py, (cuuint64_t)(L->ny + 2 * L->gy),
+                          (cuuint64_t)(L->nz + 2 * L->gz)};
+    cuuint64_t gstride[2] = {(cuuint64_t)(L->py * sizeof(R)), (cuuint64_t)(L->pz * sizeof(R))};
+    cuuint32_t box[3] = {(cuuint32_t)sp::WX, (cuuint32_t)sp::WY, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&map, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     3, const_cast<void*>(src), gdim, gstride, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    (void)x_off;
+    sp::tb_kernel<R, T><<<grid, sp::NTHREADS, smem, stream>>>(map, a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "tb_kernel launch");
+    return SP_OK;
+}
+
+template <typename R>
+int launch_tb(int T, const void* src, void* dst, const sp_layout* L, const sp::TBArgs& a, int grid,
+              cudaStream_t s) {
+    switch (T) {
+        case 1: return launch_tb_t<R, 1>(src, dst, L, a, grid, s);
+        case 2: return launch_tb_t<R, 2>(src, dst, L, a, grid, s);
+        case 3: return launch_tb_t<R, 3>(src, dst, L, a, grid, s);
+        case 4: return launch_tb_t<R, 4>(src, dst, L, a, grid, s);
+        case 5: return launch_tb_t<R, 5>(src, dst, L, a, grid, s);
+        case 6: return launch_tb_t<R, 6>(src, dst, L, a, grid, s);
+        case 7: return launch_tb_t<R, 7>(src, dst, L, a, grid, s);
+        case 8: return launch_tb_t<R, 8>(src, dst, L, a, grid, s);
+        default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sp_version(void) { return 1; }
+
+const char* sp_last_error(void) { return g_err.c_str(); }
+
+uint64_t sp_launch_count(void) { return g_launches.load(); }
+
+int sp_set_tuning(int ctas_per_sm, int chunks) {
+    int prev = g_ctas_per_sm * 1000 + g_chunks;
+    g_ctas_per_sm = ctas_per_sm;
+    g_chunks = chunks;
+    return prev;
+}
+
+int sp_layout_make(int64_t nx, int64_t ny, int64_t nz, int64_t gx, int64_t gy, int64_t gz,
+                   int dtype, sp_layout* out, int64_t* alloc_elems) {
+    int es = elem_size(dtype);
+    if (!es) return fail(SP_ERR_ARG, "unknown dtype %d", dtype);
+    if (nx < 1 || ny < 1 || nz < 1)
+        return fail(SP_ERR_GRID, "interior extents must be >= 1, got (%lld, %lld, %lld)",
+                    (long long)nx, (long long)ny, (long long)nz);
+    if (gx < 1 || gy < 1 || gz < 1) return fail(SP_ERR_GRID, "ghost width must be >= 1");
+    const int64_t align = 128 / es;  // interior row start on a 128-byte boundary
+    int64_t x_off = ((gx + align - 1) / align) * align;
+    int64_t py = ((x_off + nx + gx + align - 1) / align) * align;
+    out->nx = nx; out->ny = ny; out->nz = nz;
+    out->gx = gx; out->gy = gy; out->gz = gz;
+    out->py = py;
+    out->pz = py * (ny + 2 * gy);
+    out->origin = gz * out->pz + gy * py + x_off;
+    *alloc_elems = out->pz * (nz + 2 * gz);
+    return SP_OK;
+}
+
+int sp_fill(void* base, int dtype, const sp_layout* L, const sp_pattern* p, void* stream) {
+    int rc = check_layout(L, dtype);
+    if (rc) return rc;
+    if (!base || !p) return fail(SP_ERR_ARG, "null argument");
+    sp::FillArgs f;
+    f.nx = L->nx; f.ny = L->ny; f.nz = L->nz; f.gx = L->gx; f.gy = L->gy; f.gz = L->gz;
+    f.py = L->py; f.pz = L->pz; f.origin = L->origin;
+    f.kind = p->kind; f.has_faces = p->has_faces; f.value = p->value; f.seed = p->seed;
+    for (int i = 0; i < 3; ++i) { f.gorigin[i] = p->gorigin[i]; f.gn[i] = p->gn[i]; }
+    for (int i = 0; i < 6; ++i) f.faces[i] = p->faces[i];
+    if (p->kind < 0 || p->kind > 4) return fail(SP_ERR_GRID, "unknown fill pattern kind %d", p->kind);
+    const int64_t rows = (L->pz / L->py) * (L->nz + 2 * L->gz);
+    dim3 grid((unsigned)std::min<int64_t>(rows, 65535), (unsigned)((rows + 65534) / 65535));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == SP_F64) sp::fill_kernel<double><<<grid, 256, 0, s>>>((double*)base, f);
+    else sp::fill_kernel<float><<<grid, 256, 0, s>>>((float*)base, f);
+    g_launches.fetch_add(1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "fill_kernel launch");
+    return SP_OK;
+}
+
+int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+                     const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+                     const int32_t ext_hi[3], const int64_t out_lo[3], const int64_t out_hi[3],
+                     void* stream) {
+    int rc = check_layout(L, dtype);
+    if (rc) return rc;
+    if (!src || !dst || !lo || !hi || !out_lo || !out_hi) return fail(SP_ERR_ARG, "null argument");
+    if (src == dst) return fail(SP_ERR_ARG, "src and dst must be distinct arrays");
+    if (T < 1 || T > 8) return fail(SP_ERR_SCHEDULE, "temporal block depth T=%d outside 1..8", T);
+    const int64_t n[3] = {L->nz, L->ny, L->nx};
+    const int64_t g[3] = {L->gz, L->gy, L->gx};
+    int32_t elo[3] = {0, 0, 0}, ehi[3] = {0, 0, 0};
+    for (int d = 0; d < 3; ++d) {
+        if (ext_lo) elo[d] = ext_lo[d] ? 1 : 0;
+        if (ext_hi) ehi[d] = ext_hi[d] ? 1 : 0;
+        if (lo[d] > hi[d] || out_lo[d] > out_hi[d]) return fail(SP_ERR_GRID, "malformed region");
+        if (out_lo[d] < lo[d] || out_hi[d] > hi[d])
+            return fail(SP_ERR_GRID, "output box outside the level-T domain (axis %d)", d);
+    }
+    for (int d = 0; d < 3; ++d)
+        if (out_lo[d] == out_hi[d]) return SP_OK;  // empty box: nothing to do
+    for (int d = 0; d < 3; ++d) {
+        // the level-1 domain plus its stencil reach must stay inside the allocation
+        int64_t l1 = lo[d] - (int64_t)elo[d] * (T - 1) - 1;
+        int64_t h1 = hi[d] + (int64_t)ehi[d] * (T - 1) + 1;
+        if (l1 < -g[d] || h1 > n[d] + g[d])
+            return fail(SP_ERR_GRID, "region escapes allocation (axis %d: [%lld, %lld) with ghost %lld)",
+                        d, (long long)l1, (long long)h1, (long long)g[d]);
+    }
+    DevInfo di;
+    rc = dev_info(&di);
+    if (rc) return rc;
+
+    sp::TBArgs a;
+    a.dst = dst;
+    a.py = L->py; a.pz = L->pz; a.origin = L->origin;
+    for (int d = 0; d < 3; ++d) {
+        a.lo[d] = (int)lo[d]; a.hi[d] = (int)hi[d]; a.elo[d] = elo[d]; a.ehi[d] = ehi[d];
+        a.olo[d] = (int)out_lo[d]; a.ohi[d] = (int)out_hi[d];
+    }
+    // Output tile width: footprint minus the 2T halo; footprints start on a
+    // 16-byte boundary, so either every tile start is aligned (ox a multiple
+    // of A and lo_x - T + x_off aligned) or ox gives up A-1 cells of slack.
+    const int A = 16 / elem_size(dtype);
+    a.align = A;
+    a.x_off = (int)(L->origin - L->gz * L->pz - L->gy * L->py);
+    if (lo_x_mod(out_lo[2] - T + a.x_off, A) == 0)
+        a.ox = ((sp::WX - 2 * T) / A) * A;
+    else
+        a.ox = sp::WX - 2 * T - (A - 1);
+    a.oy = sp::WY - 2 * T;
+    a.ntx = (int)((out_hi[2] - out_lo[2] + a.ox - 1) / a.ox);
+    a.nty = (int)((out_hi[1] - out_lo[1] + a.oy - 1) / a.oy);
+    a.gy = (int)L->gy;
+    a.gz = (int)L->gz;
+    const int64_t nzb = out_hi[0] - out_lo[0];
+    const int64_t tiles = (int64_t)a.ntx * a.nty;
+    const int slots = di.sms * (g_ctas_per_sm > 0 ? g_ctas_per_sm : 1);
+    // z-chunking: minimise waves * (chunk + 2T) -- the wave-quantised cost of
+    // every unit streaming chunk+2T planes.
+    int64_t best_n = 1;
+    double best_cost = 1e300;
+    const int64_t max_chunks = std::min<int64_t>(nzb, 256);
+    for (int64_t nch = 1; nch <= max_chunks; ++nch) {
+        int64_t len = (nzb + nch - 1) / nch;
+        int64_t nreal = (nzb + len - 1) / len;
+        int64_t units = tiles * nreal;
+        double waves = (double)((units + slots - 1) / slots);
+        double cost = waves * (double)(len + 2 * T);
+        if (cost < best_cost * 0.999) { best_cost = cost; best_n = nch; }
+    }
+    if (g_chunks > 0) best_n = std::min<int64_t>(g_chunks, nzb);
+    int64_t len = (nzb + best_n - 1) / best_n;
+    int64_t nch = (nzb + len - 1) / len;
+    if (tiles * nch >= (1ll << 31)) return fail(SP_ERR_SCHEDULE, "too many work units");
+    a.chunk_len = (int)len;
+    a.units = (int)(tiles * nch);
+    int grid = (int)std::min<int64_t>(a.units, slots);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == SP_F64) return launch_tb<double>(T, src, dst, L, a, grid, s);
+    return launch_tb<float>(T, src, dst, L, a, grid, s);
+}
+
+int sp_sweep_tb(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+                const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+                const int32_t ext_hi[3], void* stream) {
+    return sp_sweep_tb_part(src, dst, dtype, L, T, lo, hi, ext_lo, ext_hi, lo, hi, stream);
+}
+
+int sp_update_region(const void* src, void* dst, int dtype, const sp_layout* L,
+                     const int64_t lo[3], const int64_t hi[3], void* stream) {
+    return sp_sweep_tb(src, dst, dtype, L, 1, lo, hi, nullptr, nullptr, stream);
+}
+
+int sp_run_sweeps(void* a, void* b, int dtype, const sp_layout* L, int64_t levels, int T,
+                  int* active, void* stream) {
+    if (!active) return fail(SP_ERR_ARG, "null active flag");
+    if (levels < 0) return fail(SP_ERR_ARG, "negative level count");
+    if (T < 1 || T > 8) return fail(SP_ERR_SCHEDULE, "temporal block depth T=%d outside 1..8", T);
+    const int64_t lo[3] = {0, 0, 0};
+    const int64_t hi[3] = {L->nz, L->ny, L->nx};
+    int act = *active ? 1 : 0;
+    while (levels > 0) {
+        int t = (int)std::min<int64_t>(T, levels);
+        void* cur = act ? b : a;
+        void* oth = act ? a : b;
+        int rc = sp_sweep_tb(cur, oth, dtype, L, t, lo, hi, nullptr, nullptr, stream);
+        if (rc) return rc;
+        act ^= 1;
+        levels -= t;
+    }
+    *active = act;
+    return SP_OK;
+}
+
+int sp_digest(const void* base, int dtype, const sp_layout* L, uint64_t* out, void* stream) {
+    int rc = check_layout(L, dtype);
+    if (rc) return rc;
+    if (!base || !out) return fail(SP_ERR_ARG, "null argument");
+    DevInfo di;
+    rc = dev_info(&di);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* d = nullptr;
+    SP_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), s));
+    SP_CUDA(cudaMemsetAsync(d, 0, sizeof(unsigned long long), s));
+    int grid = di.sms * 8;
+    if (dtype == SP_F64)
+        sp::digest_kernel<double><<<grid, 256, 0, s>>>((const double*)base, L->nx, L->ny, L->nz,
+                                                        L->py, L->pz, L->origin, d);
+    else
+        sp::digest_kernel<float><<<grid, 256, 0, s>>>((const float*)base, L->nx, L->ny, L->nz,
+                                                       L->py, L->pz, L->origin, d);
+    g_launches.fetch_add(1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "digest_kernel launch");
+    unsigned long long h = 0;
+    SP_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+    SP_CUDA(cudaFreeAsync(d, s));
+    SP_CUDA(cudaStreamSynchronize(s));
+    *out = h;
+    return SP_OK;
+}
+
+int sp_probe_fp64(double* dadd_per_s, double* ms) {
+    DevInfo di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    double* sink = nullptr;
+    SP_CUDA(cudaMalloc(&sink, 256 * sizeof(double)));
+    const int grid = di.sms * 8, block = 256, iters = 2048;
+    cudaEvent_t e0, e1;
+    SP_CUDA(cudaEventCreate(&e0));
+    SP_CUDA(cudaEventCreate(&e1));
+    sp::fp64_probe_kernel<<<grid, block>>>(1.0, iters / 8, sink);  // warm-up
+    SP_CUDA(cudaEventRecord(e0));
+    sp::fp64_probe_kernel<<<grid, block>>>(1.0, iters, sink);
+    SP_CUDA(cudaEventRecord(e1));
+    SP_CUDA(cudaEventSynchronize(e1));
+    g_launches.fetch_add(2);
+    float t = 0;
+    SP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    const double adds = (double)grid * block * iters * 64.0;
+    if (ms) *ms = t;
+    if (dadd_per_s) *dadd_per_s = adds / (t * 1e-3);
+    return SP_OK;
+}
+
+}  // extern "C"

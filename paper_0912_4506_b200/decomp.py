@@ -1,0 +1,256 @@
+"""z-slab decomposition with depth-h halos (drop-in for R/decomp.py).
+
+Geometry (``_split``, ``Decomposition``, ``level_domains_for_rank``) is the
+reference's host logic restated.  The device engine supports layouts
+(1, 1, P): ranks are z-slabs, each keeping x/y ghosts of depth 1 and z
+ghosts of depth h.  A halo exchange moves h padded z-planes to each z
+neighbour; because z is the outermost axis those planes are contiguous, so
+every message is one contiguous copy straight from the grid into the
+neighbour's ghost planes -- no pack/unpack kernel (R/grid.py:247-277 is not
+needed).  ``run_distributed`` keeps the reference's single-call,
+all-ranks-in-one-process contract (R/decomp.py:240-268, ranks as threads of
+one process); ranks are placed round-robin on the visible GPUs and exchange
+by device copies.  The multi-process NCCL engine is ``dist.SlabRunner``.
+(R = /root/reference/pkg/src/stencilpipe)
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .grid import FillPattern, GridDims, TwoGrid
+from .pipeline import DEFAULT_DEPTH, PipelineConfig, run_pass
+
+
+class DecompositionError(ValueError):
+    """Layout incompatible with the grid or the halo width (R/decomp.py:26)."""
+
+
+def _split(extent: int, parts: int) -> list[tuple[int, int]]:
+    """Near-equal 1D split; remainder to low ranks (R/decomp.py:30-39)."""
+    base, rem = divmod(extent, parts)
+    ranges = []
+    start = 0
+    for p in range(parts):
+        size = base + (1 if p < rem else 0)
+        ranges.append((start, start + size))
+        start += size
+    return ranges
+
+
+@dataclass(frozen=True)
+class Decomposition:
+    """Rank layout and halo width (R/decomp.py:42-96)."""
+    global_dims: GridDims
+    layout: tuple
+    halo: int
+
+    def __post_init__(self):
+        px, py, pz = self.layout
+        if min(px, py, pz) < 1:
+            raise DecompositionError(f"bad layout {self.layout}")
+        if self.halo < 1:
+            raise DecompositionError(f"halo width must be >= 1, got {self.halo}")
+        for p, n, name in ((px, self.global_dims.nx, "x"), (py, self.global_dims.ny, "y"),
+                           (pz, self.global_dims.nz, "z")):
+            if p > 1 and n // p < self.halo:
+                raise DecompositionError(
+                    f"{name}-split gives ranks only {n // p} cells, below the halo width {self.halo}")
+
+    @property
+    def n_ranks(self) -> int:
+        px, py, pz = self.layout
+        return px * py * pz
+
+    def coords(self, rank: int):
+        px, py, _ = self.layout
+        return (rank % px, (rank // px) % py, rank // (px * py))
+
+    def rank_of(self, cx: int, cy: int, cz: int) -> int:
+        px, py, _ = self.layout
+        return (cz * py + cy) * px + cx
+
+    def ranges(self, rank: int):
+        cx, cy, cz = self.coords(rank)
+        d = self.global_dims
+        return (_split(d.nz, self.layout[2])[cz], _split(d.ny, self.layout[1])[cy],
+                _split(d.nx, self.layout[0])[cx])
+
+    def neighbor(self, rank: int, array_axis: int, high: bool):
+        cx, cy, cz = self.coords(rank)
+        c = [cz, cy, cx]
+        p = [self.layout[2], self.layout[1], self.layout[0]]
+        c[array_axis] += 1 if high else -1
+        if not 0 <= c[array_axis] < p[array_axis]:
+            return None
+        return self.rank_of(c[2], c[1], c[0])
+
+    def local_dims(self, rank: int) -> GridDims:
+        (z0, z1), (y0, y1), (x0, x1) = self.ranges(rank)
+        return GridDims(x1 - x0, y1 - y0, z1 - z0, ghost=self.halo)
+
+
+def decompose(global_dims: GridDims, ranks: int, layout, halo: int) -> Decomposition:
+    px, py, pz = layout
+    if px * py * pz != ranks:
+        raise DecompositionError(f"layout {layout} does not factor {ranks} ranks")
+    return Decomposition(global_dims, tuple(layout), halo)
+
+
+def level_domains_for_rank(decomp: Decomposition, rank: int, h: int):
+    """Level s reaches h-s layers past every face with a neighbour (R/decomp.py:192-205)."""
+    shape = decomp.local_dims(rank).shape
+    has_low = [decomp.neighbor(rank, d, high=False) is not None for d in range(3)]
+    has_high = [decomp.neighbor(rank, d, high=True) is not None for d in range(3)]
+    domains = []
+    for s in range(1, h + 1):
+        m = h - s
+        lo = tuple(-m if has_low[d] else 0 for d in range(3))
+        hi = tuple(shape[d] + (m if has_high[d] else 0) for d in range(3))
+        domains.append((lo, hi))
+    return domains
+
+
+def _require_zslab(layout):
+    if tuple(layout[:2]) != (1, 1):
+        raise DecompositionError(
+            f"layout {tuple(layout)}: the device engine decomposes in z only (1, 1, P); "
+            "multi-axis layouts are out of scope (DESIGN.md)")
+
+
+def face_flags(decomp: Decomposition, rank: int):
+    """(ext_lo, ext_hi) per array axis: 1 where the face has a neighbour."""
+    e_lo = tuple(int(decomp.neighbor(rank, d, high=False) is not None) for d in range(3))
+    e_hi = tuple(int(decomp.neighbor(rank, d, high=True) is not None) for d in range(3))
+    return e_lo, e_hi
+
+
+def local_grid(decomp: Decomposition, rank: int, pattern, dtype=np.float64, device=None) -> TwoGrid:
+    """Rank-local device grid: z ghosts of depth h, x/y ghosts of depth 1."""
+    _require_zslab(decomp.layout)
+    origin = tuple(r[0] for r in decomp.ranges(rank))
+    dims = decomp.local_dims(rank)
+    if isinstance(pattern, FillPattern):
+        pat = pattern.shifted(origin)
+    else:
+        pat = _ShiftedPattern(pattern, origin)
+    return TwoGrid(dims, pat, dtype=dtype, device=device, ghost_xy=1, ghost_z=decomp.halo)
+
+
+class _ShiftedPattern:
+    """Duck-typed pattern in global coordinates (R/decomp.py:107-117)."""
+
+    def __init__(self, pattern, origin):
+        self._pattern = pattern
+        self._origin = tuple(origin)
+
+    def evaluate(self, lo, hi):
+        glo = tuple(l + o for l, o in zip(lo, self._origin))
+        ghi = tuple(h + o for h, o in zip(hi, self._origin))
+        return self._pattern.evaluate(glo, ghi)
+
+
+def halo_planes(grid: TwoGrid, h: int):
+    """(send_low, send_high, recv_low, recv_high) plane views of ``current``.
+
+    Each is h full padded z-planes -- one contiguous span of the allocation
+    ((ny+2)*py*h elements), sent as is.
+    """
+    return plane_spans(grid.current_buffer(), grid.layout, h)
+
+
+def plane_spans(buf, lay, h: int):
+    """Flat views of planes [0,h), [nz-h,nz), [-h,0), [nz,nz+h) of one buffer."""
+    pz, nz = lay.pz, lay.nz
+
+    def planes(z):
+        start = (z + lay.gz) * pz
+        return buf[start:start + h * pz]
+    return planes(0), planes(nz - h), planes(-h), planes(nz)
+
+
+def exchange_halos_local(grids, decomp: Decomposition, h: int) -> None:
+    """All ranks' z-halo exchange in one process (R/decomp.py:149-179, z phase).
+
+    Copies are issued after a device-wide sync of every rank's producer so a
+    cross-device copy never races the kernel that wrote its source.
+    """
+    import torch
+    for g in grids:
+        torch.cuda.synchronize(g.device)
+    views = [halo_planes(g, h) for g in grids]
+    for r, g in enumerate(grids):
+        lo_nb = decomp.neighbor(r, 0, high=False)
+        hi_nb = decomp.neighbor(r, 0, high=True)
+        if lo_nb is not None:
+            views[r][2].copy_(views[lo_nb][1], non_blocking=True)
+        if hi_nb is not None:
+            views[r][3].copy_(views[hi_nb][0], non_blocking=True)
+    for g in grids:
+        torch.cuda.synchronize(g.device)
+
+
+def outer_step(grid: TwoGrid, decomp: Decomposition, rank: int,
+               cfg: PipelineConfig | None = None, h: int | None = None) -> None:
+    """h levels on the shrinking extended domains (R/decomp.py:208-237)."""
+    if h is None:
+        if cfg is None:
+            raise DecompositionError("need either a pipeline config or h")
+        h = cfg.levels_per_sweep
+    if h != decomp.halo:
+        raise DecompositionError(f"h={h} does not match halo width {decomp.halo}")
+    if cfg is not None:
+        if cfg.storage != "twogrid":
+            raise DecompositionError("distributed runs use two-grid storage")
+        if cfg.levels_per_sweep != h:
+            raise DecompositionError(
+                f"pipeline applies U={cfg.levels_per_sweep} levels, halo is {h}")
+    depth = (cfg.depth if cfg is not None and cfg.depth else DEFAULT_DEPTH[grid.sp_dtype])
+    e_lo, e_hi = face_flags(decomp, rank)
+    shape = grid.dims.shape
+    done = 0
+    while done < h:
+        T = min(depth, h - done)
+        last = done + T
+        lo = tuple(-(h - last) * e_lo[d] for d in range(3))
+        hi = tuple(shape[d] + (h - last) * e_hi[d] for d in range(3))
+        run_pass(grid, T, lo, hi, e_lo, e_hi)
+        grid.swap()
+        done = last
+
+
+def run_distributed(global_dims: GridDims, pattern, layout, cfg: PipelineConfig | None,
+                    outer_steps: int, h: int | None = None, order=("x", "y", "z"),
+                    dtype=np.float64, devices=None):
+    """All ranks of a z-slab run in this process; returns (gathered, rank_fields).
+
+    The gathered interior equals outer_steps*h sweeps of the undecomposed
+    problem, bit for bit.  ``order`` is accepted for API parity: with
+    (1, 1, P) only the z phase carries data, so every order is equivalent.
+    """
+    import torch
+    if h is None:
+        if cfg is None:
+            raise DecompositionError("need either a pipeline config or h")
+        h = cfg.levels_per_sweep
+    px, py, pz = layout
+    decomp = decompose(global_dims, px * py * pz, layout, h)
+    _require_zslab(decomp.layout)
+    if cfg is not None and cfg.storage != "twogrid":
+        raise DecompositionError("distributed runs use two-grid storage")
+    if devices is None:
+        devices = [torch.device("cuda", i) for i in range(torch.cuda.device_count())]
+    grids = [local_grid(decomp, r, pattern, dtype=dtype, device=devices[r % len(devices)])
+             for r in range(decomp.n_ranks)]
+    for _ in range(outer_steps):
+        exchange_halos_local(grids, decomp, h)
+        for r, g in enumerate(grids):
+            outer_step(g, decomp, r, cfg, h=h)
+    rank_fields = [g.interior() for g in grids]
+    gathered = np.empty(global_dims.shape, dtype=grids[0].dtype)
+    for rank, f in enumerate(rank_fields):
+        sl = tuple(slice(lo, hi) for lo, hi in decomp.ranges(rank))
+        gathered[sl] = f
+    return gathered, rank_fields

@@ -1,0 +1,287 @@
+"""Device-resident 3D fields with ghost shells (drop-in for R/grid.py).
+
+The reference keeps a ``TwoGrid`` as two dense numpy arrays in (z, y, x)
+order (R/grid.py:121-161).  Here the pair lives in HBM, allocated by PyTorch
+with a padded row pitch so every interior row starts on a 128-byte boundary
+and TMA can stream x-y tiles (include/stencilpipe_b200.h, sp_layout_make).
+``current``/``other`` are strided torch views with the reference's
+alloc_shape; ``interior()``/``full_view()`` return host numpy copies, which is
+what ``compare`` (R/verify.py:50-53) consumes.
+(R = /root/reference/pkg/src/stencilpipe)
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+
+class GridError(ValueError):
+    """Invalid grid geometry or storage request (R/grid.py:25)."""
+
+
+@dataclass(frozen=True)
+class GridDims:
+    """Interior extents and ghost width (R/grid.py:29-51)."""
+    nx: int
+    ny: int
+    nz: int
+    ghost: int = 1
+
+    def __post_init__(self):
+        if min(self.nx, self.ny, self.nz) < 1:
+            raise GridError(f"interior extents must be >= 1, got "
+                            f"{(self.nx, self.ny, self.nz)}")
+        if self.ghost < 1:
+            raise GridError(f"ghost width must be >= 1, got {self.ghost}")
+
+    @property
+    def shape(self) -> tuple[int, int, int]:
+        return (self.nz, self.ny, self.nx)
+
+    @property
+    def alloc_shape(self) -> tuple[int, int, int]:
+        g = self.ghost
+        return tuple(n + 2 * g for n in self.shape)
+
+
+_KINDS = {"constant": 0, "linear": 1, "hotplate": 2, "random": 3, "random_pm1": 4}
+
+
+@dataclass(frozen=True)
+class FillPattern:
+    """Initial-value field over global coordinates (R/grid.py:66-118).
+
+    Evaluated on the device by K3 (``sp_fill``), bit-identical to the
+    reference's numpy evaluation.  Two extensions for the BASELINE configs:
+    kind ``random_pm1`` (2u-1, config 4) and Dirichlet ``faces`` =
+    (z-, z+, y-, y+, x-, x+) over a ``global_shape`` (z, y, x): a cell outside
+    the global interior takes the first face it lies beyond, in that order.
+    ``origin`` shifts local to global coordinates (R/decomp.py:107-117).
+    """
+
+    kind: str
+    value: float = 0.0
+    seed: int = 0
+    faces: tuple | None = None
+    global_shape: tuple | None = None
+    origin: tuple = (0, 0, 0)
+
+    def __post_init__(self):
+        if self.kind not in _KINDS:
+            raise GridError(f"unknown fill pattern {self.kind!r}")
+        if self.faces is not None and (len(self.faces) != 6 or self.global_shape is None):
+            raise GridError("faces need 6 values and a global_shape")
+
+    @classmethod
+    def constant(cls, v: float) -> "FillPattern":
+        return cls("constant", value=float(v))
+
+    @classmethod
+    def linear(cls) -> "FillPattern":
+        return cls("linear")
+
+    @classmethod
+    def hotplate(cls) -> "FillPattern":
+        return cls("hotplate")
+
+    @classmethod
+    def random(cls, seed: int) -> "FillPattern":
+        return cls("random", seed=int(seed))
+
+    @classmethod
+    def dirichlet_box(cls, kind: str, global_shape, faces, seed: int = 0,
+                      value: float = 0.0) -> "FillPattern":
+        """BASELINE-style box: ``kind`` interior, constant faces (z-,z+,y-,y+,x-,x+)."""
+        return cls(kind, value=float(value), seed=int(seed),
+                   faces=tuple(float(f) for f in faces),
+                   global_shape=tuple(int(n) for n in global_shape))
+
+    def shifted(self, origin) -> "FillPattern":
+        o = tuple(int(a) + int(b) for a, b in zip(self.origin, origin))
+        return FillPattern(self.kind, self.value, self.seed, self.faces, self.global_shape, o)
+
+    def to_c(self) -> N.Pattern:
+        p = N.Pattern()
+        p.kind = _KINDS[self.kind]
+        p.value = self.value
+        p.seed = self.seed & 0xFFFFFFFFFFFFFFFF
+        for i in range(3):
+            p.gorigin[i] = self.origin[i]
+        if self.faces is not None:
+            p.has_faces = 1
+            for i in range(3):
+                p.gn[i] = self.global_shape[i]
+            for i in range(6):
+                p.faces[i] = self.faces[i]
+        return p
+
+    def evaluate(self, lo, hi) -> np.ndarray:
+        """Host values over [lo, hi) (z, y, x), computed by the device kernel."""
+        shape = tuple(int(h - l) for l, h in zip(lo, hi))
+        if min(shape) <= 0:
+            return np.zeros(shape)
+        g = TwoGrid(GridDims(shape[2], shape[1], shape[0], 1), self.shifted(lo), _init_b=False)
+        return g.interior()
+
+
+def _torch_dtype(dtype):
+    import torch
+    if dtype in (None, np.float64, "float64", "f64", "fp64") or dtype is torch.float64:
+        return torch.float64, N.SP_F64
+    if dtype in (np.float32, "float32", "f32", "fp32") or dtype is torch.float32:
+        return torch.float32, N.SP_F32
+    if isinstance(dtype, np.dtype):
+        return _torch_dtype(dtype.type)
+    raise GridError(f"unsupported dtype {dtype!r} (float64 or float32)")
+
+
+class TwoGrid:
+    """Ping-pong pair in HBM; ``active`` selects the current level (R/grid.py:121-161).
+
+    ``ghost_xy``/``ghost_z`` override the physical ghost depth per axis group
+    (z-slab ranks keep depth-h halos in z only; x/y ghosts beyond depth 1 are
+    never read by a 6-neighbour stencil).
+    """
+
+    storage = "twogrid"
+
+    def __init__(self, dims: GridDims, pattern, dtype=np.float64, device=None,
+                 ghost_xy: int | None = None, ghost_z: int | None = None,
+                 _init_b: bool = True):
+        import torch
+        L = N.lib()
+        self.dims = dims
+        self.pattern = pattern
+        self.torch_dtype, self.sp_dtype = _torch_dtype(dtype)
+        self.dtype = np.float64 if self.sp_dtype == N.SP_F64 else np.float32
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        gxy = dims.ghost if ghost_xy is None else int(ghost_xy)
+        gz = dims.ghost if ghost_z is None else int(ghost_z)
+        lay = N.Layout()
+        n_alloc = ctypes.c_int64()
+        N.check(L.sp_layout_make(dims.nx, dims.ny, dims.nz, gxy, gxy, gz, self.sp_dtype,
+                                 ctypes.byref(lay), ctypes.byref(n_alloc)))
+        self.layout = lay
+        self.gxy, self.gz = gxy, gz
+        with torch.cuda.device(self.device):
+            self._a = torch.zeros(n_alloc.value, dtype=self.torch_dtype, device=self.device)
+            self._b = torch.empty_like(self._a)
+        self._fill(pattern)
+        if _init_b:
+            self._b.copy_(self._a)
+        self.active = 0
+
+    # -- storage -------------------------------------------------------------
+
+    def stream(self):
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _view(self, buf):
+        lay = self.layout
+        size = (lay.nz + 2 * self.gz, lay.ny + 2 * self.gxy, lay.nx + 2 * self.gxy)
+        off = lay.origin - self.gz * lay.pz - self.gxy * lay.py - self.gxy
+        return buf.as_strided(size, (lay.pz, lay.py, 1), off)
+
+    def _fill(self, pattern):
+        if isinstance(pattern, FillPattern):
+            with _on(self.device):
+                N.check(N.lib().sp_fill(ctypes.c_void_p(self._a.data_ptr()), self.sp_dtype,
+                                        ctypes.byref(self.layout), ctypes.byref(pattern.to_c()),
+                                        self.stream()))
+            return
+        if not hasattr(pattern, "evaluate"):
+            raise GridError(f"pattern {pattern!r} has no evaluate(lo, hi)")
+        # duck-typed pattern (R/grid.py:126-133): evaluate on the host, upload once
+        import torch
+        lo = (-self.gz, -self.gxy, -self.gxy)
+        hi = (self.dims.nz + self.gz, self.dims.ny + self.gxy, self.dims.nx + self.gxy)
+        vals = np.asarray(pattern.evaluate(lo, hi), dtype=self.dtype)
+        self._view(self._a).copy_(torch.from_numpy(np.ascontiguousarray(vals)))
+
+    @property
+    def buffers(self):
+        """(a, b) flat device buffers -- the raw allocations the C ABI receives."""
+        return self._a, self._b
+
+    @property
+    def current(self):
+        return self._view(self._a if self.active == 0 else self._b)
+
+    @property
+    def other(self):
+        return self._view(self._b if self.active == 0 else self._a)
+
+    def current_buffer(self):
+        return self._a if self.active == 0 else self._b
+
+    def other_buffer(self):
+        return self._b if self.active == 0 else self._a
+
+    def arrays(self):
+        return (self.current, self.other)
+
+    def swap(self) -> None:
+        self.active ^= 1
+
+    # -- host views ----------------------------------------------------------
+
+    def interior_device(self):
+        gz, g = self.gz, self.gxy
+        d = self.dims
+        return self.current[gz:gz + d.nz, g:g + d.ny, g:g + d.nx]
+
+    def interior(self) -> np.ndarray:
+        return self.interior_device().cpu().numpy()
+
+    def full_view(self) -> np.ndarray:
+        return self.current.cpu().numpy()
+
+    def value_at(self, i: int, j: int, k: int) -> float:
+        g = self.dims.ghost
+        for idx, n in zip((i, j, k), (self.dims.nx, self.dims.ny, self.dims.nz)):
+            if not -g <= idx < n + g:
+                raise IndexError(f"index {(i, j, k)} outside interior+ghost range")
+        return float(self.current[k + self.gz, j + self.gxy, i + self.gxy].item())
+
+    def digest(self) -> int:
+        """64-bit digest of the current interior (definition: oracle/jacobi_oracle.c)."""
+        out = ctypes.c_uint64()
+        with _on(self.device):
+            N.check(N.lib().sp_digest(ctypes.c_void_p(self.current_buffer().data_ptr()),
+                                      self.sp_dtype, ctypes.byref(self.layout),
+                                      ctypes.byref(out), self.stream()))
+        return int(out.value)
+
+
+class _on:
+    """Make ``device`` current for the duration of a C-ABI call."""
+
+    def __init__(self, device):
+        self.device = device
+
+    def __enter__(self):
+        import torch
+        self._ctx = torch.cuda.device(self.device)
+        self._ctx.__enter__()
+
+    def __exit__(self, *a):
+        self._ctx.__exit__(*a)
+
+
+def allocate(dims: GridDims, mode: str, pattern, slack: int = 0, **kw):
+    """Allocate and initialise a device grid (R/grid.py:217-223); two-grid only."""
+    if mode == "twogrid":
+        return TwoGrid(dims, pattern, **kw)
+    if mode == "compressed":
+        raise GridError("compressed storage is not implemented on the device "
+                        "(A/B ping-pong is the B200 layout; see DESIGN.md)")
+    raise GridError(f"unknown storage mode {mode!r}")

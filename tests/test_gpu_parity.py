@@ -1,0 +1,256 @@
+"""Device parity: every result compared bit-for-bit with the reference goldens
+(tests/golden, produced by the reference package itself) or with the pinned
+C oracle on identical seeded inputs.
+
+fp64 tolerance: bitwise (north_star: <=1e-13 relative, bit-exact when the
+reference's summation order is kept -- it is).  fp32 tolerance: <=1e-5
+relative per north_star, and we additionally assert bitwise.
+"""
+
+import itertools
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+Z1 = (1.0, 0.0, 0.0, 0.0, 0.0, 0.0)
+C3F = (1.0, 0.0, 0.5, 0.0, 0.25, 0.0)
+
+
+def dims_of(sp, shape, ghost=1):
+    return sp.GridDims(shape[2], shape[1], shape[0], ghost)
+
+
+def oracle_run(O, shape, kind, seed, faces, levels, dtype=np.float64):
+    g = O.CGrid(shape, O.BoxPattern(kind, seed=seed, faces=faces,
+                                    global_shape=shape if faces else None), dtype=dtype)
+    g.sweeps(levels)
+    return g
+
+
+def bitwise(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and a.dtype == b.dtype and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+# ---- K3 fill ------------------------------------------------------------------
+
+def test_fill_matches_reference_hash(sp, kat):
+    pat = sp.FillPattern.random(0)
+    for key, bits in kat["random0_bits"].items():
+        c = tuple(int(v) for v in key.split(","))
+        v = pat.evaluate(c, tuple(i + 1 for i in c))[0, 0, 0]
+        assert np.float64(v).view(np.uint64) == bits, key
+
+
+def test_fill_faced_box_matches_reference(sp, ref_fields):
+    shape = (17, 19, 21)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, C3F))
+    assert bitwise(g.full_view(), ref_fields["c3like_21x19x17_full0"])
+    # B is a copy of A including the ghost shell (R/grid.py:132-133)
+    assert bitwise(g.other.cpu().numpy(), g.full_view())
+
+
+def test_c1_initial_digest(sp, kat):
+    shape = (128, 128, 128)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, Z1))
+    assert g.digest() == kat["c1_digest_l0"]
+
+
+# ---- reference known answers ------------------------------------------------------
+
+def test_hotplate_first_sweep_golden(sp, ref_fields):
+    g = sp.TwoGrid(sp.GridDims(4, 4, 4), sp.FillPattern.hotplate())
+    sp.sweep_naive(g)
+    expected = np.zeros((4, 4, 4))
+    expected[:, :, 0] = 1.0 / 6.0
+    assert bitwise(g.interior(), expected)
+    assert bitwise(g.interior(), ref_fields["hotplate4_l1"])
+
+
+@pytest.mark.parametrize("kind", ["constant", "linear"])
+def test_fixed_points(sp, kind):
+    pat = sp.FillPattern.constant(3.5) if kind == "constant" else sp.FillPattern.linear()
+    g = sp.TwoGrid(sp.GridDims(16, 16, 16), pat)
+    start = g.interior().copy()
+    sp.sweeps(g, 64, depth=4)
+    assert bitwise(g.interior(), start)
+
+
+def test_trajectory_every_level(sp, ref_fields):
+    traj = ref_fields["r11_16_traj"]
+    g = sp.TwoGrid(sp.GridDims(16, 16, 16), sp.FillPattern.random(11))
+    assert bitwise(g.interior(), traj[0])
+    for lv in range(1, 9):
+        sp.sweep_naive(g)
+        assert bitwise(g.interior(), traj[lv]), lv
+
+
+@pytest.mark.parametrize("depth", range(1, 9))
+def test_trajectory_temporal_blocking(sp, ref_fields, depth):
+    traj = ref_fields["r11_16_traj"]
+    for levels in (depth, 8):
+        g = sp.TwoGrid(sp.GridDims(16, 16, 16), sp.FillPattern.random(11))
+        sp.sweeps(g, levels, depth=depth)
+        assert bitwise(g.interior(), traj[levels]), (depth, levels)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3, 4, 5, 8])
+def test_ragged_and_degenerate(sp, ref_fields, depth):
+    g = sp.TwoGrid(sp.GridDims(9, 7, 5), sp.FillPattern.random(2))
+    sp.sweeps(g, 7, depth=depth)
+    assert bitwise(g.interior(), ref_fields["r2_9x7x5_l7"])
+    g = sp.TwoGrid(sp.GridDims(1, 3, 2), sp.FillPattern.random(3))
+    sp.sweeps(g, 3, depth=depth)
+    assert bitwise(g.interior(), ref_fields["r3_1x3x2_l3"])
+
+
+def test_pipeline_config_u16(sp, ref_fields):
+    g = sp.TwoGrid(sp.GridDims(24, 24, 24), sp.FillPattern.random(11))
+    cfg = sp.PipelineConfig(teams=2, team_size=4, updates_per_thread=2, block=(24, 16, 16))
+    sp.run_node_sweeps(g, cfg, 1)
+    assert bitwise(g.interior(), ref_fields["r11_24_pipe_u16"])
+
+
+@pytest.mark.parametrize("depth", range(1, 9))
+def test_faced_boxes(sp, ref_fields, depth):
+    shape = (20, 18, 33)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, Z1))
+    sp.sweeps(g, 12, depth=depth)
+    assert bitwise(g.interior(), ref_fields["c1like_33x18x20_l12"])
+    shape = (17, 19, 21)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, C3F))
+    sp.sweeps(g, 9, depth=depth)
+    assert bitwise(g.interior(), ref_fields["c3like_21x19x17_l9"])
+
+
+@pytest.mark.parametrize("depth", range(1, 9))
+def test_float32(sp, ref_fields, depth):
+    shape = (24, 20, 36)
+    pat = sp.FillPattern.dirichlet_box("random_pm1", shape, (0.0,) * 6)
+    g = sp.TwoGrid(dims_of(sp, shape), pat, dtype=np.float32)
+    sp.sweeps(g, 10, depth=depth)
+    got, ref = g.interior(), ref_fields["c4like_f32_36x20x24_l10"]
+    assert got.dtype == np.float32
+    cmp = sp.compare(ref, got, tol=sp.F32_REL_TOL)   # north_star fp32 tolerance 1e-5
+    assert cmp.passed, str(cmp)
+    assert cmp.bitwise, str(cmp)
+
+
+def test_ghost_shell_never_written(sp):
+    shape = (13, 11, 19)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, C3F))
+    a0 = g.current.cpu().numpy().copy()
+    sp.sweeps(g, 11, depth=4)
+    for arr in (g.current.cpu().numpy(), g.other.cpu().numpy()):
+        shell = np.ones(arr.shape, bool)
+        shell[1:-1, 1:-1, 1:-1] = False
+        assert bitwise(arr[shell], a0[shell])
+
+
+def test_update_block_level_parity(sp, O):
+    shape = (6, 6, 6)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.random(13))
+    sp.update_block(g, (0, 0, 0), shape, level=1)
+    sp.update_block(g, (0, 0, 0), shape, level=2)
+    ref = oracle_run(O, shape, "random", 13, None, 2)
+    assert bitwise(g.interior(), ref.interior())
+
+
+def test_update_block_subbox_matches_oracle(sp, O):
+    shape = (9, 10, 11)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.random(5))
+    ref = O.CGrid(shape, O.BoxPattern("random", seed=5))
+    for lo, hi in [((0, 0, 0), (4, 10, 11)), ((2, 3, 1), (7, 9, 5)), ((0, 0, 0), (1, 1, 1))]:
+        sp.update_block(g, lo, hi, level=1)
+        ref.update_region(lo, hi, level=1)
+        assert bitwise(g.other.cpu().numpy(), ref.b if ref.active == 0 else ref.a)
+
+
+def test_update_block_bounds(sp):
+    g = sp.TwoGrid(sp.GridDims(4, 4, 4), sp.FillPattern.constant(0.0))
+    with pytest.raises(sp.GridError):
+        sp.update_block(g, (0, 0, 0), (5, 4, 4))
+    with pytest.raises(sp.GridError):
+        sp.update_block(g, (2, 0, 0), (1, 4, 4))
+
+
+def test_schedule_errors(sp):
+    g = sp.TwoGrid(sp.GridDims(4, 4, 4), sp.FillPattern.constant(0.0))
+    with pytest.raises(sp.ScheduleError):
+        sp.run_node_sweeps(g, sp.PipelineConfig(teams=1, team_size=1, updates_per_thread=5), 1)
+
+
+# ---- randomised parity vs the pinned C oracle ----------------------------------------
+
+CASES = [((1, 1, 1), 3, 1), ((2, 3, 5), 5, 2), ((17, 32, 64), 9, 4), ((40, 70, 130), 8, 8),
+         ((33, 31, 29), 7, 3), ((64, 24, 56), 8, 4), ((5, 100, 9), 6, 6), ((70, 65, 190), 10, 5)]
+
+
+@pytest.mark.parametrize("shape,levels,depth", CASES)
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_random_shapes_vs_oracle(sp, O, shape, levels, depth, dtype):
+    seed = sum(shape) * 7 + levels
+    faces = (0.3, -1.0, 2.0, 0.0, 1.0, -0.5)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, faces, seed=seed),
+                   dtype=dtype)
+    sp.sweeps(g, levels, depth=depth)
+    ref = oracle_run(O, shape, "random", seed, faces, levels, dtype=dtype)
+    assert bitwise(g.interior(), ref.interior()), (shape, levels, depth)
+
+
+# ---- sub-box passes (the overlap split) --------------------------------------------
+
+@pytest.mark.parametrize("T", [1, 3, 4, 8])
+def test_partial_boxes_compose(sp, T):
+    shape = (40, 30, 50)
+    pat = sp.FillPattern.dirichlet_box("random", shape, C3F)
+    full = sp.TwoGrid(dims_of(sp, shape), pat)
+    sp.pipeline.run_pass(full, T, (0, 0, 0), shape)
+    split = sp.TwoGrid(dims_of(sp, shape), pat)
+    nz = shape[0]
+    for olo, ohi in [((0, 0, 0), (T, 30, 50)), ((nz - T, 0, 0), (nz, 30, 50)),
+                     ((T, 0, 0), (nz - T, 30, 50))]:
+        sp.pipeline.run_pass(split, T, (0, 0, 0), shape, out_lo=olo, out_hi=ohi)
+    assert bitwise(full.other.cpu().numpy(), split.other.cpu().numpy())
+
+
+# ---- distributed z-slabs (single process, ranks share the GPU) -----------------------
+
+@pytest.mark.parametrize("case", ["dist_P2_h1_s3", "dist_P2_h4_s2", "dist_P3_h2_s2",
+                                  "dist_P4_h4_s2", "dist_P4_h8_s1"])
+def test_distributed_matches_reference(sp, kat, ref_fields, case):
+    c = kat["dist_cases"][case]
+    gd = sp.GridDims(12, 10, 40)
+    pat = sp.FillPattern.dirichlet_box("random", (40, 10, 12), Z1)
+    gathered, fields = sp.run_distributed(gd, pat, (1, 1, c["P"]), cfg=None,
+                                          outer_steps=c["steps"], h=c["h"])
+    assert bitwise(gathered, ref_fields[case])
+
+
+def test_distributed_pipelined_depth_split(sp, ref_fields):
+    # h=8 with depth 3: three passes per outer step over extended domains
+    gd = sp.GridDims(12, 10, 40)
+    pat = sp.FillPattern.dirichlet_box("random", (40, 10, 12), Z1)
+    cfg = sp.PipelineConfig(teams=1, team_size=4, updates_per_thread=2, depth=3)
+    gathered, _ = sp.run_distributed(gd, pat, (1, 1, 4), cfg, outer_steps=1)
+    assert bitwise(gathered, ref_fields["dist_P4_h8_s1"])
+
+
+def test_distributed_rejects_multi_axis(sp):
+    with pytest.raises(sp.DecompositionError):
+        sp.run_distributed(sp.GridDims(16, 16, 16), sp.FillPattern.random(1), (2, 1, 1), None, 1, h=1)
+
+
+# ---- C1: the BASELINE parity config ----------------------------------------------------
+
+def test_c1_full_grid_vs_reference(sp, kat, ref_fields):
+    shape = (128, 128, 128)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, Z1))
+    cfg = sp.PipelineConfig(teams=1, team_size=1, updates_per_thread=4, depth=4)   # T=4
+    sp.run_node_sweeps(g, cfg, 25)                                                 # 100 sweeps
+    assert g.digest() == kat["c1_digest_l100"]
+    inner = g.interior()
+    assert bitwise(inner[kat["c1_planes_index"]], ref_fields["c1_planes_l100"])
