@@ -124,9 +124,12 @@ int sp_digest(const void* base, int dtype, const sp_layout* L, uint64_t* out,
  * compute roof of the stencil, which has no fusable multiply-add. */
 int sp_probe_fp64(double* dadd_per_s, double* ms);
 
-/* Tuning hook: number of resident CTAs per SM the scheduler assumes (0 =
- * auto) and z-chunk override (0 = auto).  Returns the previous values. */
-int sp_set_tuning(int ctas_per_sm, int chunks);
+/* Tuning hook (benchmarks only): kernel-variant override (0 = automatic per
+ * dtype/T; k = variant k-1 of {16x2/2, 16x2/3, 8x4/2, 8x4/3, 8x8/2, 16x4/2}
+ * = warps x rows-per-thread / z-queue slots; a variant not built for a depth
+ * falls back to the first) and z-chunk count override (0 = automatic).
+ * Returns the previous values encoded as variant*1000 + chunks. */
+int sp_set_tuning(int variant, int chunks);
 
 #ifdef __cplusplus
 }

@@ -18,7 +18,7 @@ import sys
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_NAME = "libstencilpipe_b200.so"
-LIB_PATH = os.path.join(_HERE, LIB_NAME)
+LIB_PATH = os.environ.get("SP_LIB_PATH") or os.path.join(_HERE, LIB_NAME)
 SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "jacobi_kernels.cuh")]
 HEADER = os.path.join(_ROOT, "include", "stencilpipe_b200.h")
 
@@ -57,27 +57,30 @@ class Pattern(ctypes.Structure):
                 ("faces", ctypes.c_double * 6)]
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, out: str | None = None,
+          defines=()) -> str:
     """Compile the sm_100a library in-tree with nvcc; returns its path."""
+    target = out or LIB_PATH
     newest = max(os.path.getmtime(p) for p in SOURCES + [HEADER])
-    if not force and os.path.exists(LIB_PATH) and os.path.getmtime(LIB_PATH) >= newest:
-        return LIB_PATH
+    if not force and not defines and os.path.exists(target) and os.path.getmtime(target) >= newest:
+        return target
     nvcc = os.environ.get("NVCC", "nvcc")
     if not any(os.access(os.path.join(p, "nvcc"), os.X_OK)
                for p in os.environ.get("PATH", "").split(os.pathsep)):
         if os.path.exists("/usr/local/cuda/bin/nvcc"):
             nvcc = "/usr/local/cuda/bin/nvcc"
-    tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, "-o", tmp, os.path.join(_HERE, "csrc", "capi.cu")]
+    tmp = target + ".tmp"
+    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp,
+           os.path.join(_HERE, "csrc", "capi.cu")]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed:\n{res.stderr}")
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB_PATH)
-    with open(os.path.join(_HERE, "csrc", "ptxas.log"), "w") as fh:
+    os.replace(tmp, target)
+    with open(target + ".ptxas.log" if out else os.path.join(_HERE, "csrc", "ptxas.log"), "w") as fh:
         fh.write(res.stderr)
-    return LIB_PATH
+    return target
 
 
 _lib = None

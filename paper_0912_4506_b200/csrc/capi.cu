@@ -18,7 +18,6 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
-int g_ctas_per_sm = 0;
 int g_chunks = 0;
 
 int fail(int code, const char* fmt, ...) {
@@ -89,52 +88,160 @@ int check_layout(const sp_layout* L, int dtype) {
     return SP_OK;
 }
 
-template <typename R, int T>
-int launch_tb_t(const void* src, void* dst, const sp_layout* L, const sp::TBArgs& a, int grid,
-                cudaStream_t stream) {
-    constexpr int PLANE = sp::WX * sp::WY;
-    constexpr int NLVL = (T > 1) ? (T - 1) : 1;
-    const size_t smem = (size_t)(sp::RING + NLVL) * PLANE * sizeof(R) + sp::RING * sizeof(uint64_t);
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        SP_CUDA(cudaFuncSetAttribute(sp::tb_kernel<R, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-        attr_set = true;
+// Kernel variants: CTA shape (warps BY x rows-per-thread PY; footprint is
+// 64 x BY*PY) and z-queue depth (2 = shift by moves, 3 = rotating registers).
+struct Variant {
+    int by, py, slots;
+};
+constexpr Variant kVariants[] = {{16, 2, 2}, {16, 2, 3}, {8, 4, 2}, {8, 4, 3}, {8, 8, 2}, {16, 4, 2}};
+constexpr int kNumVariants = 6;
+int g_variant_override = -1;
+
+// Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
+// (16x2, 2 slots) fits every depth and is the fallback.
+template <typename R, int T, int V>
+constexpr bool compiled() {
+    if (V == 0) return true;
+    if (sizeof(R) == 8) {
+        if (T == 1) return V == 1;
+        if (T == 2) return V == 1 || V == 3 || V == 4;
+        if (T == 3) return V == 2 || V == 3;
+        if (T == 4) return V == 2 || V == 3;
+        return false;
     }
-    auto enc = encode_fn();
-    if (!enc) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
-    CUtensorMap map;
-    const int64_t x_off = L->origin - L->gz * L->pz - L->gy * L->py;
-    cuuint64_t gdim[3] = {(cuuint64_t)L->py, (cuuint64_t)(L->ny + 2 * L->gy),
-                          (cuuint64_t)(L->nz + 2 * L->gz)};
-    cuuint64_t gstride[2] = {(cuuint64_t)(L->py * sizeof(R)), (cuuint64_t)(L->pz * sizeof(R))};
-    cuuint32_t box[3] = {(cuuint32_t)sp::WX, (cuuint32_t)sp::WY, 1};
-    cuuint32_t estr[3] = {1, 1, 1};
-    CUresult r = enc(&map, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                     3, const_cast<void*>(src), gdim, gstride, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    (void)x_off;
-    sp::tb_kernel<R, T><<<grid, sp::NTHREADS, smem, stream>>>(map, a);
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "tb_kernel launch");
-    return SP_OK;
+    if (T == 1) return V == 1;
+    if (T == 2) return V == 1 || V == 3 || V == 4;
+    if (T <= 4) return V == 2 || V == 3 || V == 4;
+    return V == 2;
+}
+
+// Default variant per (dtype, T), from the B200 tuning runs (DESIGN.md,
+// profiles/tuning_r01.md): fp64 T=2 16x2/3, T=3 8x4/3, T=4 8x4/2; fp32 T<=2
+// 16x2, T=3..4 8x8/2, deeper 8x4/2.
+int default_variant(int dtype, int T) {
+    if (dtype == SP_F64) {
+        if (T == 1) return 1;
+        if (T == 2) return 1;
+        if (T == 3) return 3;
+        if (T == 4) return 2;
+        return 0;
+    }
+    if (T <= 2) return T == 1 ? 1 : 0;
+    if (T <= 4) return 4;
+    return 2;
+}
+
+// Host mirror of sp::Plan<>::FITS.
+bool variant_fits(int dtype, int T, int v) {
+    const int es = elem_size(dtype);
+    const int wy = kVariants[v].by * kVariants[v].py;
+    const int plane = sp::WX * wy * es, budget = 232448 - 256, nl = T > 1 ? T - 1 : 0;
+    const int nbuf = (2 * nl + 3) * plane <= budget ? 2 : 1;
+    int ring = budget / plane - nbuf * nl;
+    if (ring > 8) ring = 8;
+    return ring >= 3 && wy - 2 * T >= 1;
+}
+
+template <typename R, int T, int V>
+constexpr bool usable() {
+    constexpr Variant v = kVariants[V];
+    return compiled<R, T, V>() && sp::Plan<R, T, v.by, v.py, v.slots>::FITS;
+}
+
+template <typename R, int T>
+bool is_usable(int v) {
+    switch (v) {
+        case 0: return usable<R, T, 0>();
+        case 1: return usable<R, T, 1>();
+        case 2: return usable<R, T, 2>();
+        case 3: return usable<R, T, 3>();
+        case 4: return usable<R, T, 4>();
+        default: return usable<R, T, 5>();
+    }
 }
 
 template <typename R>
-int launch_tb(int T, const void* src, void* dst, const sp_layout* L, const sp::TBArgs& a, int grid,
+bool usable_rt(int T, int v) {
+    switch (T) {
+        case 1: return is_usable<R, 1>(v);
+        case 2: return is_usable<R, 2>(v);
+        case 3: return is_usable<R, 3>(v);
+        case 4: return is_usable<R, 4>(v);
+        case 5: return is_usable<R, 5>(v);
+        case 6: return is_usable<R, 6>(v);
+        case 7: return is_usable<R, 7>(v);
+        default: return is_usable<R, 8>(v);
+    }
+}
+
+int variant_for(int dtype, int T) {
+    int v = default_variant(dtype, T);
+    if (g_variant_override >= 0 && g_variant_override < kNumVariants) v = g_variant_override;
+    bool ok = dtype == SP_F64 ? usable_rt<double>(T, v) : usable_rt<float>(T, v);
+    return ok ? v : 0;
+}
+
+template <typename R, int T, int V>
+int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
+                cudaStream_t stream) {
+    if constexpr (!usable<R, T, V>()) {
+        return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
+    } else {
+        constexpr Variant v = kVariants[V];
+        using Pl = sp::Plan<R, T, v.by, v.py, v.slots>;
+        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots>;
+        const size_t smem = Pl::SMEM;
+        static bool attr_set = false;  // per instantiation
+        if (!attr_set) {
+            SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr_set = true;
+        }
+        auto enc = encode_fn();
+        if (!enc) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+        CUtensorMap map;
+        cuuint64_t gdim[3] = {(cuuint64_t)L->py, (cuuint64_t)(L->ny + 2 * L->gy),
+                              (cuuint64_t)(L->nz + 2 * L->gz)};
+        cuuint64_t gstride[2] = {(cuuint64_t)(L->py * sizeof(R)), (cuuint64_t)(L->pz * sizeof(R))};
+        cuuint32_t box[3] = {(cuuint32_t)sp::WX, (cuuint32_t)Pl::WY, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = enc(&map, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         3, const_cast<void*>(src), gdim, gstride, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+        kern<<<grid, Pl::NT, smem, stream>>>(map, a);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "tb_kernel launch");
+        return SP_OK;
+    }
+}
+
+template <typename R, int T>
+int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
+                   cudaStream_t s) {
+    switch (v) {
+        case 0: return launch_tb_t<R, T, 0>(src, L, a, grid, s);
+        case 1: return launch_tb_t<R, T, 1>(src, L, a, grid, s);
+        case 2: return launch_tb_t<R, T, 2>(src, L, a, grid, s);
+        case 3: return launch_tb_t<R, T, 3>(src, L, a, grid, s);
+        case 4: return launch_tb_t<R, T, 4>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 5>(src, L, a, grid, s);
+    }
+}
+
+template <typename R>
+int launch_tb(int T, int v, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
               cudaStream_t s) {
     switch (T) {
-        case 1: return launch_tb_t<R, 1>(src, dst, L, a, grid, s);
-        case 2: return launch_tb_t<R, 2>(src, dst, L, a, grid, s);
-        case 3: return launch_tb_t<R, 3>(src, dst, L, a, grid, s);
-        case 4: return launch_tb_t<R, 4>(src, dst, L, a, grid, s);
-        case 5: return launch_tb_t<R, 5>(src, dst, L, a, grid, s);
-        case 6: return launch_tb_t<R, 6>(src, dst, L, a, grid, s);
-        case 7: return launch_tb_t<R, 7>(src, dst, L, a, grid, s);
-        case 8: return launch_tb_t<R, 8>(src, dst, L, a, grid, s);
+        case 1: return launch_variant<R, 1>(v, src, L, a, grid, s);
+        case 2: return launch_variant<R, 2>(v, src, L, a, grid, s);
+        case 3: return launch_variant<R, 3>(v, src, L, a, grid, s);
+        case 4: return launch_variant<R, 4>(v, src, L, a, grid, s);
+        case 5: return launch_variant<R, 5>(v, src, L, a, grid, s);
+        case 6: return launch_variant<R, 6>(v, src, L, a, grid, s);
+        case 7: return launch_variant<R, 7>(v, src, L, a, grid, s);
+        case 8: return launch_variant<R, 8>(v, src, L, a, grid, s);
         default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
     }
 }
@@ -149,9 +256,9 @@ const char* sp_last_error(void) { return g_err.c_str(); }
 
 uint64_t sp_launch_count(void) { return g_launches.load(); }
 
-int sp_set_tuning(int ctas_per_sm, int chunks) {
-    int prev = g_ctas_per_sm * 1000 + g_chunks;
-    g_ctas_per_sm = ctas_per_sm;
+int sp_set_tuning(int variant, int chunks) {
+    int prev = (g_variant_override + 1) * 1000 + g_chunks;
+    g_variant_override = variant - 1;   // 0 = automatic, k = variant k-1
     g_chunks = chunks;
     return prev;
 }
@@ -248,14 +355,17 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
         a.ox = ((sp::WX - 2 * T) / A) * A;
     else
         a.ox = sp::WX - 2 * T - (A - 1);
-    a.oy = sp::WY - 2 * T;
+    const int variant = variant_for(dtype, T);
+    const int wy = kVariants[variant].by * kVariants[variant].py;
+    if (wy - 2 * T < 1) return fail(SP_ERR_SCHEDULE, "depth T=%d too deep for a %d-row footprint", T, wy);
+    a.oy = wy - 2 * T;
     a.ntx = (int)((out_hi[2] - out_lo[2] + a.ox - 1) / a.ox);
     a.nty = (int)((out_hi[1] - out_lo[1] + a.oy - 1) / a.oy);
     a.gy = (int)L->gy;
     a.gz = (int)L->gz;
     const int64_t nzb = out_hi[0] - out_lo[0];
     const int64_t tiles = (int64_t)a.ntx * a.nty;
-    const int slots = di.sms * (g_ctas_per_sm > 0 ? g_ctas_per_sm : 1);
+    const int slots = di.sms;
     // z-chunking: minimise waves * (chunk + 2T) -- the wave-quantised cost of
     // every unit streaming chunk+2T planes.
     int64_t best_n = 1;
@@ -277,8 +387,8 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
     a.units = (int)(tiles * nch);
     int grid = (int)std::min<int64_t>(a.units, slots);
     cudaStream_t s = (cudaStream_t)stream;
-    if (dtype == SP_F64) return launch_tb<double>(T, src, dst, L, a, grid, s);
-    return launch_tb<float>(T, src, dst, L, a, grid, s);
+    if (dtype == SP_F64) return launch_tb<double>(T, variant, src, L, a, grid, s);
+    return launch_tb<float>(T, variant, src, L, a, grid, s);
 }
 
 int sp_sweep_tb(const void* src, void* dst, int dtype, const sp_layout* L, int T,

@@ -1,23 +1,25 @@
-// jacobi_tb.cu -- sm_100a kernels for the temporally blocked 3D Jacobi sweep.
+// jacobi_kernels.cuh -- sm_100a kernels for the temporally blocked 3D Jacobi sweep.
 //
-// K2 `tb_kernel<R, T>`: one CTA owns an x-y footprint of WX x WY cells
-// (output tile + T-cell halo each side) and marches it through z.  Level-0
-// planes stream in by TMA (cp.async.bulk.tensor.3d) into a RING-deep
+// K2 `tb_kernel<R, T, BY, PY>`: one CTA owns an x-y footprint of WX x WY
+// cells (output tile + T-cell halo each side) and marches it through z.
+// Level-0 planes stream in by TMA (cp.async.bulk.tensor.3d) into a RING-deep
 // shared-memory ring guarded by mbarriers; levels 1..T are a register
 // pipeline, one z-plane per level per step, level t lagging level t-1 by one
 // plane (the z-wavefront).  The reference's per-level block shift
 // (R/pipeline.py:165-182, shift -(tau-1)) is exactly this lag in z.
 //
-// Per thread: a 2x2 patch of columns (PX=2 in x, PY=2 in y).  x-neighbours
-// come from the adjacent lane by shuffle, y-neighbours across warps from a
-// per-level shared-memory plane; z-neighbours are the thread's own registers.
-// Per column and level the registers hold  m = v[p-1], c = v[p] and
-// s = (x- + x+) + (y- + y+) at plane p, so every update is
-//     v_t[p] = (s + (v_{t-1}[p-1] + v_{t-1}[p+1])) * ONE_SIXTH
+// Per thread: a PX x PY patch of columns (PX=2 in x, PY rows in y); the CTA
+// is 32 lanes (x) by BY warps (y), WX = 64, WY = BY*PY.  Neighbours inside a
+// patch come from the thread's registers, x-neighbours across lanes by
+// shuffle, y-neighbours across warps from a per-level shared-memory plane
+// (only a patch's first and last rows are ever stored), z-neighbours from the
+// thread's own z-queue.  Per column and level the registers hold
+// m = v[p-1] and c = v[p]; each update is
+//     v_t[p] = (((x- + x+) + (y- + y+)) + (v_{t-1}[p-1] + v_{t-1}[p+1])) * ONE_SIXTH
 // in the reference's summation order (R/kernel.py:27-34), with explicit
 // __dadd_rn/__dmul_rn (no FMA contraction) -> bit-identical to numpy.
 //
-// K1 (a single level over any box, R/kernel.py:37-40) is tb_kernel<R,1>.
+// K1 (a single level over any box, R/kernel.py:37-40) is tb_kernel<R,1,...>.
 // K3 `fill_kernel` initialises a grid from the coordinate hash
 // (R/grid.py:54-118).  K5 `digest_kernel` reduces the interior to the 64-bit
 // digest the oracle defines.
@@ -26,17 +28,13 @@
 #include <cudaTypedefs.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace sp {
 
-constexpr int BX = 32;            // lanes along x (one warp = one footprint row pair)
-constexpr int BY = 16;            // warps along y
-constexpr int PX = 2;             // columns per thread in x
-constexpr int PY = 2;             // columns per thread in y
-constexpr int WX = BX * PX;       // footprint width  (64 cells)
-constexpr int WY = BY * PY;       // footprint height (32 cells)
-constexpr int NTHREADS = BX * BY; // 512
-constexpr int RING = 4;           // TMA ring depth (level-0 planes in flight)
-constexpr int NCOL = PX * PY;
+constexpr int BX = 32;            // lanes along x
+constexpr int PX = 2;             // columns per thread in x (one 16/8-byte vector)
+constexpr int WX = BX * PX;       // footprint width (64 cells)
 
 struct TBArgs {
     void* dst;                 // allocation base of the destination grid
@@ -135,18 +133,41 @@ __device__ __forceinline__ int footprint_x(const TBArgs& a, int x0, int T) {
     return x0 - T - r;
 }
 
-template <typename R, int T>
-__global__ void __launch_bounds__(NTHREADS, 1)
+// Shared-memory plan per instantiation: a RING-deep TMA ring of level-0
+// planes plus, for levels 1..T-1, one plane each -- double-buffered when it
+// fits (one barrier per step), single-buffered otherwise (two barriers).
+template <typename R, int T, int BY, int PY, int SLOTS = 3>
+struct Plan {
+    static_assert(T * PY <= 64 && T * PX <= 32, "domain bitmasks too narrow");
+    static constexpr int WY = BY * PY;
+    static constexpr int NT = 32 * BY;
+    static constexpr int PLANE = WX * WY;
+    static constexpr int PLANE_BYTES = PLANE * (int)sizeof(R);
+    static constexpr int BUDGET = 232448 - 256;             // opt-in smem per CTA, minus barriers
+    static constexpr int NL = (T > 1) ? (T - 1) : 0;        // stored level planes
+    static constexpr bool DB = (2 * NL + 3) * PLANE_BYTES <= BUDGET;
+    static constexpr int NBUF = DB ? 2 : 1;
+    static constexpr int RING_FIT = BUDGET / PLANE_BYTES - NBUF * NL;
+    static constexpr int RING = RING_FIT > 8 ? 8 : RING_FIT;
+    static constexpr bool FITS = RING >= 3 && WY - 2 * T >= 1;
+    static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + RING * 8;
+};
+
+template <typename R, int T, int BY, int PY, int SLOTS>
+__global__ void __launch_bounds__(32 * BY, 1)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
+    static_assert(SLOTS == 2 || SLOTS == 3, "z-queue slots");
     using A = Arith<R>;
     using V2 = typename A::V2;
-    constexpr int PLANE = WX * WY;
-    constexpr int NLVL = (T > 1) ? (T - 1) : 1;
+    using P = Plan<R, T, BY, PY, SLOTS>;
+    constexpr int WY = P::WY;
+    constexpr int PLANE = P::PLANE;
+    constexpr int RING_N = P::RING;
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     R* ring = reinterpret_cast<R*>(smem_raw);
-    R* lvl = ring + RING * PLANE;                                     // levels 1..T-1
-    uint64_t* full = reinterpret_cast<uint64_t*>(lvl + NLVL * PLANE);  // RING mbarriers
+    R* lvl = ring + RING_N * PLANE;  // [level-1][buf] planes for levels 1..T-1
+    uint64_t* full = reinterpret_cast<uint64_t*>(lvl + P::NBUF * P::NL * PLANE);
 
     const int lane = threadIdx.x & 31;
     const int wy = threadIdx.x >> 5;
@@ -154,10 +175,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int cy = wy * PY;    // footprint-local y of the thread's first row
     const int cym = max(cy - 1, 0);
     const int cyp = min(cy + PY, WY - 1);
-    constexpr uint32_t kPlaneBytes = PLANE * sizeof(R);
+    constexpr uint32_t kPlaneBytes = P::PLANE_BYTES;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < RING; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < RING_N; ++i) mbar_init(&full[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -180,7 +201,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     };
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-        for (int i = 0; i < RING; ++i) produce(i);
+        for (int i = 0; i < RING_N - 1; ++i) produce(i);   // slot RING-1 is filled after step 0
     }
 
     const R sixth = A::sixth();
@@ -191,110 +212,207 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int fx = footprint_x(a, w.x0, T), fy = w.y0 - T;
         const int nsteps = (w.zc1 - w.zc0) + 2 * T;
 
-        // xy part of each level's domain, one bit per (level, column).
-        uint32_t xym = 0;
+        // Per-level x/y domain of this thread's columns: x bits (PX per level)
+        // and y bits (PY per level); `fastm` bit t-1 = every cell of this
+        // WARP lies in level t's x/y domain (then the Dirichlet select is
+        // skipped warp-uniformly).
+        uint32_t xin = 0;
+        uint64_t yin = 0;   // T*PY bits (up to 64)
+        uint32_t fastm = 0;
 #pragma unroll
         for (int t = 1; t <= T; ++t) {
             int xl = a.lo[2] - a.elo[2] * (T - t), xh = a.hi[2] + a.ehi[2] * (T - t);
             int yl = a.lo[1] - a.elo[1] * (T - t), yh = a.hi[1] + a.ehi[1] * (T - t);
+            bool all = true;
 #pragma unroll
-            for (int k = 0; k < NCOL; ++k) {
-                int gx = fx + cx + (k % PX), gyy = fy + cy + (k / PX);
-                if (gx >= xl && gx < xh && gyy >= yl && gyy < yh) xym |= 1u << ((t - 1) * NCOL + k);
+            for (int i = 0; i < PX; ++i) {
+                int gx = fx + cx + i;
+                bool in = gx >= xl && gx < xh;
+                all &= in;
+                if (in) xin |= 1u << ((t - 1) * PX + i);
             }
-        }
-        // level-T write mask: inside this tile's output region and the box.
-        uint32_t wm = 0;
 #pragma unroll
-        for (int k = 0; k < NCOL; ++k) {
-            int gx = fx + cx + (k % PX), gyy = fy + cy + (k / PX);
-            bool in = gx >= w.x0 && gx < min(w.x0 + a.ox, a.ohi[2]) && gyy >= w.y0 &&
-                      gyy < min(w.y0 + a.oy, a.ohi[1]);
-            wm |= (in ? 1u : 0u) << k;
+            for (int j = 0; j < PY; ++j) {
+                int gyy = fy + cy + j;
+                bool in = gyy >= yl && gyy < yh;
+                all &= in;
+                if (in) yin |= 1ull << ((t - 1) * PY + j);
+            }
+            if (__all_sync(0xffffffffu, all)) fastm |= 1u << (t - 1);
+        }
+        // level-T write masks: inside this tile's output region and the box.
+        uint32_t wx = 0, wyb = 0;
+#pragma unroll
+        for (int i = 0; i < PX; ++i) {
+            int gx = fx + cx + i;
+            wx |= (gx >= w.x0 && gx < min(w.x0 + a.ox, a.ohi[2]) ? 1u : 0u) << i;
+        }
+#pragma unroll
+        for (int j = 0; j < PY; ++j) {
+            int gyy = fy + cy + j;
+            wyb |= (gyy >= w.y0 && gyy < min(w.y0 + a.oy, a.ohi[1]) ? 1u : 0u) << j;
         }
         R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
+        // both x cells written and the pair 16-byte aligned (same for every row: py is)
+        const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
 
-        R m[T][NCOL], c[T][NCOL], s[T][NCOL];  // level t-1 state / level-t partial sums
+        // Per level t < T, a register z-queue.  SLOTS == 3: three slots
+        // rotating with the step phase -- at phase f, Q[f] = v[p-1],
+        // Q[f+1] = v[p], and the new plane v[p+1] lands in Q[f+2]; steps are
+        // unrolled by 3, so there are no register moves.  SLOTS == 2: Q[0] =
+        // v[p-1], Q[1] = v[p], the new plane lives in a transient and the
+        // queue shifts by moves (fewer live registers, more instructions).
+        R Q[SLOTS][T][PY][PX];
 #pragma unroll
-        for (int t = 0; t < T; ++t)
+        for (int f = 0; f < SLOTS; ++f)
 #pragma unroll
-            for (int k = 0; k < NCOL; ++k) m[t][k] = c[t][k] = s[t][k] = R(0);
+            for (int t = 0; t < T; ++t)
+#pragma unroll
+                for (int j = 0; j < PY; ++j)
+#pragma unroll
+                    for (int i = 0; i < PX; ++i) Q[f][t][j][i] = R(0);
 
-        for (int st = 0; st < nsteps; ++st, ++gstep) {
-            const int slot = gstep % RING;
-            mbar_wait(&full[slot], (gstep / RING) & 1);
-            const R* L0 = ring + slot * PLANE;
+        // One z-step.  FAST (warp-uniform, decided per step): every cell of
+        // the warp is inside every level's domain this step, so the update is
+        // straight-line; otherwise cells outside D_t keep their previous-level
+        // value (Dirichlet walls, rank faces) through a per-cell select.
+        auto step = [&](auto phase, auto fast, int st) {
+            constexpr int F0 = SLOTS == 3 ? decltype(phase)::value : 0;    // v[p-1]
+            constexpr int F1 = SLOTS == 3 ? (F0 + 1) % 3 : 1;              // v[p]
+            constexpr int F2 = SLOTS == 3 ? (F0 + 2) % 3 : 0;              // v[p+1] (3 slots)
+            constexpr bool FAST = decltype(fast)::value;
+            const int slot = gstep % RING_N;
+            const int pslot = (gstep + RING_N - 1) % RING_N;
+            const int cur = P::DB ? (int)(gstep & 1u) : 0;
+            const int prv = P::DB ? cur ^ 1 : 0;
             const int q = w.zc0 - T + st;
 
-            // ---- phase A: advance every level by one plane -----------------
-            R n[NCOL];
-            {
-                V2 r0 = *reinterpret_cast<const V2*>(L0 + cy * WX + cx);
-                V2 r1 = *reinterpret_cast<const V2*>(L0 + (cy + 1) * WX + cx);
-                n[0] = r0.x; n[1] = r0.y; n[2] = r1.x; n[3] = r1.y;
-            }
-#pragma unroll
-            for (int t = 1; t <= T; ++t) {
-                R nn[NCOL];
-                const int p = q - t;
-                const bool zin = p >= a.lo[0] - a.elo[0] * (T - t) && p < a.hi[0] + a.ehi[0] * (T - t);
-#pragma unroll
-                for (int k = 0; k < NCOL; ++k) {
-                    bool in = zin && ((xym >> ((t - 1) * NCOL + k)) & 1u);
-                    R upd = A::mul(A::add(s[t - 1][k], A::add(m[t - 1][k], n[k])), sixth);
-                    nn[k] = in ? upd : c[t - 1][k];
-                }
-#pragma unroll
-                for (int k = 0; k < NCOL; ++k) {
-                    m[t - 1][k] = c[t - 1][k];
-                    c[t - 1][k] = n[k];
-                    n[k] = nn[k];
-                }
-                if (t < T) {
-                    R* P = lvl + (t - 1) * PLANE;
-                    *reinterpret_cast<V2*>(P + cy * WX + cx) = V2{n[0], n[1]};
-                    *reinterpret_cast<V2*>(P + (cy + 1) * WX + cx) = V2{n[2], n[3]};
-                }
-            }
-            // level T: write the finished plane (only once the pipeline is full)
-            if (st >= 2 * T) {
-                const int p = q - T;
-                R* d = dcol + (int64_t)p * a.pz;
+            // s_t = (x- + x+) + (y- + y+) of level t-1 at plane q-t, produced in
+            // the previous step (ring slot pslot / level buffer prv; own and
+            // lane-neighbour cells from the registers of Q[F1]).
+            R s[T][PY][PX];
+            auto xy_sums = [&](int t) {
+                const R* Pl = (t == 1) ? ring + pslot * PLANE : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
+                const R(&v)[PY][PX] = Q[F1][t - 1];
+                V2 up = *reinterpret_cast<const V2*>(Pl + cym * WX + cx);
+                V2 dn = *reinterpret_cast<const V2*>(Pl + cyp * WX + cx);
 #pragma unroll
                 for (int j = 0; j < PY; ++j) {
-                    R* dr = d + j * a.py;
-                    bool w0 = (wm >> (j * PX)) & 1u, w1 = (wm >> (j * PX + 1)) & 1u;
-                    if (w0 && w1 && ((reinterpret_cast<uintptr_t>(dr) & (sizeof(V2) - 1)) == 0)) {
-                        *reinterpret_cast<V2*>(dr) = V2{n[j * PX], n[j * PX + 1]};
-                    } else {
-                        if (w0) dr[0] = n[j * PX];
-                        if (w1) dr[1] = n[j * PX + 1];
+                    R lft = __shfl_up_sync(0xffffffffu, v[j][1], 1);
+                    R rgt = __shfl_down_sync(0xffffffffu, v[j][0], 1);
+                    R ym0 = (j == 0) ? up.x : v[j > 0 ? j - 1 : 0][0];
+                    R ym1 = (j == 0) ? up.y : v[j > 0 ? j - 1 : 0][1];
+                    R yp0 = (j == PY - 1) ? dn.x : v[j + 1 < PY ? j + 1 : j][0];
+                    R yp1 = (j == PY - 1) ? dn.y : v[j + 1 < PY ? j + 1 : j][1];
+                    s[t - 1][j][0] = A::add(A::add(lft, v[j][1]), A::add(ym0, yp0));
+                    s[t - 1][j][1] = A::add(A::add(v[j][0], rgt), A::add(ym1, yp1));
+                }
+            };
+            if constexpr (!P::DB) {
+#pragma unroll
+                for (int t = 1; t <= T; ++t) xy_sums(t);
+                __syncthreads();   // single buffers: all reads before any overwrite
+            }
+
+            mbar_wait(&full[slot], (gstep / RING_N) & 1);
+            // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
+            R Nt[SLOTS == 3 ? 1 : T][PY][PX];
+            auto newv = [&](int t) -> R(&)[PY][PX] {
+                if constexpr (SLOTS == 3) return Q[F2][t];
+                else return Nt[t];
+            };
+            {
+                const R* L0 = ring + slot * PLANE;
+                R(&n0)[PY][PX] = newv(0);
+#pragma unroll
+                for (int j = 0; j < PY; ++j) {
+                    V2 r = *reinterpret_cast<const V2*>(L0 + (cy + j) * WX + cx);
+                    n0[j][0] = r.x;
+                    n0[j][1] = r.y;
+                }
+            }
+            R out[PY][PX];  // level-T values of plane q-T
+#pragma unroll
+            for (int t = 1; t <= T; ++t) {
+                if constexpr (P::DB) xy_sums(t);
+                const R(&mm)[PY][PX] = Q[F0][t - 1];
+                const R(&cc)[PY][PX] = Q[F1][t - 1];
+                const R(&nn)[PY][PX] = newv(t - 1);
+                R(&dst)[PY][PX] = (t < T) ? newv(t < T ? t : 0) : out;
+                uint32_t inm = 0;   // SLOW: one bit per cell, in D_t this step
+                if constexpr (!FAST) {
+                    const int p = q - t;
+                    const bool zin = p >= a.lo[0] - a.elo[0] * (T - t) && p < a.hi[0] + a.ehi[0] * (T - t);
+                    const uint32_t xb = (xin >> ((t - 1) * PX)) & ((1u << PX) - 1);
+                    const uint32_t yb = (uint32_t)(yin >> ((t - 1) * PY)) & ((1u << PY) - 1);
+#pragma unroll
+                    for (int j = 0; j < PY; ++j)
+                        if (zin && ((yb >> j) & 1u)) inm |= xb << (j * PX);
+                }
+#pragma unroll
+                for (int j = 0; j < PY; ++j)
+#pragma unroll
+                    for (int i = 0; i < PX; ++i) {
+                        R upd = A::mul(A::add(s[t - 1][j][i], A::add(mm[j][i], nn[j][i])), sixth);
+                        if constexpr (FAST) dst[j][i] = upd;
+                        else dst[j][i] = ((inm >> (j * PX + i)) & 1u) ? upd : cc[j][i];
+                        if constexpr (SLOTS == 2) {   // shift level t-1's queue
+                            Q[0][t - 1][j][i] = cc[j][i];
+                            Q[1][t - 1][j][i] = nn[j][i];
+                        }
+                    }
+                if (t < T) {
+                    R* Pl = lvl + ((t - 1) * P::NBUF + cur) * PLANE;
+                    *reinterpret_cast<V2*>(Pl + cy * WX + cx) = V2{dst[0][0], dst[0][1]};
+                    if (PY > 1)
+                        *reinterpret_cast<V2*>(Pl + (cy + PY - 1) * WX + cx) =
+                            V2{dst[PY - 1][0], dst[PY - 1][1]};
+                }
+            }
+            // level T: write the finished plane (once the pipeline is full)
+            if (st >= 2 * T) {
+                R* d = dcol + (int64_t)(q - T) * a.pz;
+                if (vec_store) {
+#pragma unroll
+                    for (int j = 0; j < PY; ++j)
+                        if ((wyb >> j) & 1u) *reinterpret_cast<V2*>(d + j * a.py) = V2{out[j][0], out[j][1]};
+                } else {
+#pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        const bool row = (wyb >> j) & 1u;
+                        if (row && (wx & 1u)) d[j * a.py] = out[j][0];
+                        if (row && (wx & 2u)) d[j * a.py + 1] = out[j][1];
                     }
                 }
             }
             __syncthreads();
-
-            // ---- phase B: x-y partial sums for the next step ---------------
-#pragma unroll
-            for (int t = 0; t < T; ++t) {
-                const R* P = (t == 0) ? L0 : (lvl + (t - 1) * PLANE);
-                const R* v = c[t];  // plane just produced by level t
-                V2 up = *reinterpret_cast<const V2*>(P + cym * WX + cx);
-                V2 dn = *reinterpret_cast<const V2*>(P + cyp * WX + cx);
-                R l0 = __shfl_up_sync(0xffffffffu, v[1], 1);
-                R l1 = __shfl_up_sync(0xffffffffu, v[3], 1);
-                R r0 = __shfl_down_sync(0xffffffffu, v[0], 1);
-                R r1 = __shfl_down_sync(0xffffffffu, v[2], 1);
-                s[t][0] = A::add(A::add(l0, v[1]), A::add(up.x, v[2]));
-                s[t][1] = A::add(A::add(v[0], r0), A::add(up.y, v[3]));
-                s[t][2] = A::add(A::add(l1, v[3]), A::add(v[0], dn.x));
-                s[t][3] = A::add(A::add(v[2], r1), A::add(v[1], dn.y));
-            }
-            __syncthreads();
+            // ring slot pslot (read for level 1's sums this step) is free now
             if (threadIdx.x == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                produce(slot);
+                produce(pslot);
             }
+            ++gstep;
+        };
+        // warp-uniform: the whole warp is inside every level's x/y domain
+        const bool fast_xy = fastm == (1u << T) - 1u;
+        // planes q-t of every level inside its z domain
+        auto zin_all = [&](int st) {
+            const int q = w.zc0 - T + st;
+            return q - 1 < a.hi[0] + a.ehi[0] * (T - 1) && q - T >= a.lo[0];
+        };
+        auto run = [&](auto phase, int st) {
+            if (fast_xy && zin_all(st)) step(phase, std::true_type{}, st);
+            else step(phase, std::false_type{}, st);
+        };
+
+        if constexpr (SLOTS == 3) {
+            for (int st = 0; st < nsteps; st += 3) {
+                run(std::integral_constant<int, 0>{}, st);
+                if (st + 1 < nsteps) run(std::integral_constant<int, 1>{}, st + 1);
+                if (st + 2 < nsteps) run(std::integral_constant<int, 2>{}, st + 2);
+            }
+        } else {
+            for (int st = 0; st < nsteps; ++st) run(std::integral_constant<int, 0>{}, st);
         }
     }
 }

@@ -20,7 +20,7 @@ from .grid import GridDims, TwoGrid, _on
 
 # Levels fused per HBM pass when the config does not say (tuned on B200;
 # see DESIGN.md "Choice of T").
-DEFAULT_DEPTH = {N.SP_F64: 4, N.SP_F32: 4}
+DEFAULT_DEPTH = {N.SP_F64: 2, N.SP_F32: 4}
 MAX_DEPTH = 8
 
 

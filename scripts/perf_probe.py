@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--levels", type=int, default=24)
     ap.add_argument("--depths", default="1,2,3,4,5,6,8")
     ap.add_argument("--chunks", type=int, default=0)
+    ap.add_argument("--shapes", default="0", help="comma list: 0=auto, k=shape k-1")
     args = ap.parse_args()
     dt = np.float64 if args.dtype == "f64" else np.float32
     n = args.n
@@ -32,14 +33,14 @@ def main():
     shape = (nz, n, n)
     pat = sp.FillPattern.dirichlet_box("random", shape, (1.0, 0, 0.5, 0, 0.25, 0))
     g = sp.TwoGrid(sp.GridDims(n, n, nz), pat, dtype=dt)
-    if args.chunks:
-        sp._native.lib().sp_set_tuning(0, args.chunks)
     out = {}
     rate = ctypes.c_double()
     ms = ctypes.c_double()
     sp._native.check(sp._native.lib().sp_probe_fp64(ctypes.byref(rate), ctypes.byref(ms)))
     out["fp64_dadd_per_s"] = rate.value
-    for depth in [int(d) for d in args.depths.split(",")]:
+    for shape in [int(v) for v in args.shapes.split(",")]:
+      sp._native.lib().sp_set_tuning(shape, args.chunks)
+      for depth in [int(d) for d in args.depths.split(",")]:
         levels = (args.levels // depth) * depth
         sp.sweeps(g, depth, depth=depth)   # warm-up (JIT attr, TMA descriptors)
         torch.cuda.synchronize()
@@ -52,9 +53,9 @@ def main():
         t = e0.elapsed_time(e1) / 1e3
         glups = n * n * nz * levels / t / 1e9
         es = 8 if dt == np.float64 else 4
-        out[f"T{depth}"] = {"glups": round(glups, 1), "ms_per_pass": round(t / (levels // depth) * 1e3, 3),
+        out[f"S{shape}T{depth}"] = {"glups": round(glups, 1), "ms_per_pass": round(t / (levels // depth) * 1e3, 3),
                             "hbm_equiv_gbs": round(glups * 2 * es / depth, 1)}
-        print(depth, out[f"T{depth}"], flush=True)
+        print(shape, depth, out[f"S{shape}T{depth}"], flush=True)
     print(json.dumps(out))
 
 

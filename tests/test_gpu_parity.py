@@ -254,3 +254,22 @@ def test_c1_full_grid_vs_reference(sp, kat, ref_fields):
     assert g.digest() == kat["c1_digest_l100"]
     inner = g.interior()
     assert bitwise(inner[kat["c1_planes_index"]], ref_fields["c1_planes_l100"])
+
+
+@pytest.mark.parametrize("shape_id", [1, 2, 3, 4])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_every_cta_shape(sp, O, shape_id, dtype):
+    lib = sp._native.lib()
+    lib.sp_set_tuning(shape_id, 0)
+    try:
+        for shape, levels, depth in [((40, 70, 130), 8, 4), ((33, 31, 29), 7, 3), ((70, 65, 190), 10, 2),
+                                     ((20, 18, 33), 8, 8), ((9, 80, 70), 5, 5)]:
+            seed = sum(shape) + levels
+            faces = (0.3, -1.0, 2.0, 0.0, 1.0, -0.5)
+            g = sp.TwoGrid(dims_of(sp, shape),
+                           sp.FillPattern.dirichlet_box("random", shape, faces, seed=seed), dtype=dtype)
+            sp.sweeps(g, levels, depth=depth)
+            ref = oracle_run(O, shape, "random", seed, faces, levels, dtype=dtype)
+            assert bitwise(g.interior(), ref.interior()), (shape_id, shape, depth)
+    finally:
+        lib.sp_set_tuning(0, 0)
