@@ -116,9 +116,12 @@ int sp_run_sweeps(void* a, void* b, int dtype, const sp_layout* L, int64_t level
                   int T, int* active, void* stream);
 
 /* K5: order-independent 64-bit digest of the interior (definition in
- * oracle/jacobi_oracle.c).  Synchronises the stream. */
-int sp_digest(const void* base, int dtype, const sp_layout* L, uint64_t* out,
-              void* stream);
+ * oracle/jacobi_oracle.c), cell (z,y,x) hashed with linear index
+ * index_base + (z*ny + y)*nx + x -- so the digests of a z-slab decomposition
+ * (index_base = z0*ny*nx per slab) sum to the digest of the whole grid.
+ * Synchronises the stream. */
+int sp_digest(const void* base, int dtype, const sp_layout* L, int64_t index_base,
+              uint64_t* out, void* stream);
 
 /* Measured FP64 add throughput of this device (DADD/s over all SMs) -- the
  * compute roof of the stencil, which has no fusable multiply-add. */

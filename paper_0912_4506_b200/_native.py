@@ -110,7 +110,7 @@ def load_library():
                                    i32p, i32p, i64p, i64p, vp]
     L.sp_run_sweeps.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int64, ctypes.c_int,
                                 P(ctypes.c_int), vp]
-    L.sp_digest.argtypes = [vp, ctypes.c_int, P(Layout), P(ctypes.c_uint64), vp]
+    L.sp_digest.argtypes = [vp, ctypes.c_int, P(Layout), ctypes.c_int64, P(ctypes.c_uint64), vp]
     L.sp_probe_fp64.argtypes = [P(ctypes.c_double), P(ctypes.c_double)]
     L.sp_set_tuning.argtypes = [ctypes.c_int, ctypes.c_int]
     for name in EXPORTS:

@@ -423,7 +423,8 @@ int sp_run_sweeps(void* a, void* b, int dtype, const sp_layout* L, int64_t level
     return SP_OK;
 }
 
-int sp_digest(const void* base, int dtype, const sp_layout* L, uint64_t* out, void* stream) {
+int sp_digest(const void* base, int dtype, const sp_layout* L, int64_t index_base, uint64_t* out,
+              void* stream) {
     int rc = check_layout(L, dtype);
     if (rc) return rc;
     if (!base || !out) return fail(SP_ERR_ARG, "null argument");
@@ -437,10 +438,10 @@ int sp_digest(const void* base, int dtype, const sp_layout* L, uint64_t* out, vo
     int grid = di.sms * 8;
     if (dtype == SP_F64)
         sp::digest_kernel<double><<<grid, 256, 0, s>>>((const double*)base, L->nx, L->ny, L->nz,
-                                                        L->py, L->pz, L->origin, d);
+                                                        L->py, L->pz, L->origin, index_base, d);
     else
         sp::digest_kernel<float><<<grid, 256, 0, s>>>((const float*)base, L->nx, L->ny, L->nz,
-                                                       L->py, L->pz, L->origin, d);
+                                                       L->py, L->pz, L->origin, index_base, d);
     g_launches.fetch_add(1);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "digest_kernel launch");

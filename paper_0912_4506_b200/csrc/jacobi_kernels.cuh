@@ -485,13 +485,13 @@ __global__ void fill_kernel(R* base, const FillArgs f) {
 
 template <typename R>
 __global__ void digest_kernel(const R* base, int64_t nx, int64_t ny, int64_t nz, int64_t py,
-                              int64_t pz, int64_t origin, unsigned long long* out) {
+                              int64_t pz, int64_t origin, int64_t index_base, unsigned long long* out) {
     const int64_t rows = ny * nz;
     uint64_t acc = 0;
     for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
         int64_t z = row / ny, y = row - (row / ny) * ny;
         const R* r = base + origin + z * pz + y * py;
-        uint64_t idx = (uint64_t)row * (uint64_t)nx;
+        uint64_t idx = (uint64_t)index_base + (uint64_t)row * (uint64_t)nx;
         for (int64_t x = threadIdx.x; x < nx; x += blockDim.x) {
             uint64_t bits;
             if (sizeof(R) == 8) bits = (uint64_t)__double_as_longlong((double)r[x]);

@@ -69,6 +69,7 @@ class SlabRunner:
         # overlap needs one pass per outer step and a non-empty interior slab
         self.overlap = overlap and h <= min(self.depth, MAX_DEPTH) and nz > 2 * h
         self._pending = []
+        self._primed = False
         self.messages = 0
         self.bytes_sent = 0
 
@@ -106,40 +107,52 @@ class SlabRunner:
 
     # -- compute -------------------------------------------------------------
 
-    def _levels(self, first_done, T):
-        h = self.h
-        last = first_done + T
+    def _domain(self, levels, done, T):
+        """Final-level domain of a pass reaching level done+T of a ``levels`` step."""
+        last = done + T
         shape = self.grid.dims.shape
-        lo = tuple(-(h - last) * self.e_lo[d] for d in range(3))
-        hi = tuple(shape[d] + (h - last) * self.e_hi[d] for d in range(3))
+        lo = tuple(-(levels - last) * self.e_lo[d] for d in range(3))
+        hi = tuple(shape[d] + (levels - last) * self.e_hi[d] for d in range(3))
         return lo, hi
 
-    def step(self):
-        """One outer step: h levels; halos of the new state posted if overlapping."""
+    def step(self, levels: int | None = None):
+        """One outer step of ``levels`` <= h levels (default h).
+
+        Overlapped: wait for the halos of the current state, run K2 on the two
+        boundary slabs (the h planes each neighbour needs next), post their
+        transfer, then run K2 on the interior slab while NCCL moves them.
+        """
         g, h = self.grid, self.h
-        if not self.overlap:
-            self.exchange()
+        r = h if levels is None else int(levels)
+        if not 1 <= r <= h:
+            raise DecompositionError(f"step of {r} levels needs 1 <= levels <= h={h}")
+        if not self.overlap or r > self.depth:
+            if self._primed:
+                self._wait()
+            else:
+                self.exchange()
+            self._primed = False
             done = 0
-            while done < h:
-                T = min(self.depth, h - done)
-                lo, hi = self._levels(done, T)
+            while done < r:
+                T = min(self.depth, r - done)
+                lo, hi = self._domain(r, done, T)
                 self.engine.run_pass(g, T, lo, hi, self.e_lo, self.e_hi, lo, hi)
                 g.swap()
                 done += T
             return
-        if not self._pending and not getattr(self, "_primed", False):
-            self._post(g.current_buffer())          # first step: halos of S_0
-        self._primed = True
+        if not self._primed:
+            self._post(g.current_buffer())          # halos of the current state
+            self._primed = True
         self._wait()
-        lo, hi = self._levels(0, h)
+        lo, hi = self._domain(r, 0, r)
         nz = g.dims.nz
         low = ((0, lo[1], lo[2]), (h, hi[1], hi[2]))
         high = ((nz - h, lo[1], lo[2]), (nz, hi[1], hi[2]))
         inner = ((h, lo[1], lo[2]), (nz - h, hi[1], hi[2]))
         for olo, ohi in (low, high):
-            self.engine.run_pass(g, h, lo, hi, self.e_lo, self.e_hi, olo, ohi)
-        self._post(g.other_buffer())                 # boundary planes of S_{k+1}
-        self.engine.run_pass(g, h, lo, hi, self.e_lo, self.e_hi, *inner)
+            self.engine.run_pass(g, r, lo, hi, self.e_lo, self.e_hi, olo, ohi)
+        self._post(g.other_buffer())                 # boundary planes of the new state
+        self.engine.run_pass(g, r, lo, hi, self.e_lo, self.e_hi, *inner)
         g.swap()
 
     def run(self, outer_steps: int):

@@ -252,12 +252,16 @@ class TwoGrid:
                 raise IndexError(f"index {(i, j, k)} outside interior+ghost range")
         return float(self.current[k + self.gz, j + self.gxy, i + self.gxy].item())
 
-    def digest(self) -> int:
-        """64-bit digest of the current interior (definition: oracle/jacobi_oracle.c)."""
+    def digest(self, index_base: int = 0) -> int:
+        """64-bit digest of the current interior (definition: oracle/jacobi_oracle.c).
+
+        ``index_base`` offsets the cell index, so the digests of the z-slabs of
+        a decomposition (index_base = z0*ny*nx) add up (mod 2^64) to the
+        digest of the gathered grid."""
         out = ctypes.c_uint64()
         with _on(self.device):
             N.check(N.lib().sp_digest(ctypes.c_void_p(self.current_buffer().data_ptr()),
-                                      self.sp_dtype, ctypes.byref(self.layout),
+                                      self.sp_dtype, ctypes.byref(self.layout), int(index_base),
                                       ctypes.byref(out), self.stream()))
         return int(out.value)
 

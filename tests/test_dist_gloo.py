@@ -1,0 +1,86 @@
+"""Multi-process z-slab halo exchange on CPU: world_size 2 (and 3), gloo backend.
+
+Runs paper_0912_4506_b200.dist.SlabRunner -- the same exchange/overlap logic
+bench.py uses with NCCL -- over a test-only host engine (tests/hostengine.py)
+and checks the gathered field bit-for-bit against the reference's own
+run_distributed output (tests/golden, R/decomp.py:240-268) and the oracle.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+Z1 = (1.0, 0.0, 0.0, 0.0, 0.0, 0.0)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, h, steps, overlap, levels, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import torch.distributed as dist
+    from hostengine import HostEngine
+    from oracle import oracle as O
+    import paper_0912_4506_b200 as sp
+    from paper_0912_4506_b200.dist import SlabRunner
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gshape = (40, 10, 12)
+        base = O.BoxPattern("random", seed=0, faces=Z1, global_shape=gshape)
+        r = SlabRunner(sp.GridDims(12, 10, 40), None, h=h, dtype=np.float64, depth=h,
+                       engine=HostEngine(base), overlap=overlap)
+        for lv in levels or [h] * steps:
+            r.step(levels=lv)
+        r.finish()
+        full = r.gather()
+        if rank == 0:
+            q.put((full, r.overlap, r.messages))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, h, steps, overlap=True, levels=None):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, h, steps, overlap, levels, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("h,steps", [(1, 3), (4, 2)])
+def test_two_ranks_match_reference(ref_fields, kat, h, steps, overlap):
+    full, did_overlap, msgs = _run(2, h, steps, overlap)
+    ref = ref_fields[f"dist_P2_h{h}_s{steps}"]
+    assert full.shape == ref.shape
+    assert np.array_equal(full.view(np.uint64), ref.view(np.uint64))
+    assert did_overlap == overlap
+    assert msgs > 0
+
+
+def test_three_ranks_with_remainder_step(O):
+    # 2 steps of h=4 then a 3-level remainder step: 11 levels in total
+    full, _, _ = _run(3, 4, 0, True, levels=[4, 4, 3])
+    g = O.CGrid((40, 10, 12), O.BoxPattern("random", seed=0, faces=Z1, global_shape=(40, 10, 12)))
+    g.sweeps(11)
+    assert np.array_equal(full.view(np.uint64), g.interior().view(np.uint64))

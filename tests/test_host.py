@@ -1,0 +1,130 @@
+"""Host-side logic (no GPU): API mirrors, schedules, decomposition geometry,
+and the C ABI library's exported surface."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_library_exports_every_declared_symbol(sp):
+    hdr = open(os.path.join(ROOT, "include", "stencilpipe_b200.h")).read()
+    declared = set(re.findall(r"^\w[\w\s\*]*?\b(sp_\w+)\(", hdr, flags=re.M))
+    assert declared == set(sp._native.EXPORTS)
+    L = sp._native.load_library()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.sp_version() == 1
+
+
+def test_layout_policy(sp):
+    L = sp._native.load_library()
+    lay = sp._native.Layout()
+    n = ctypes.c_int64()
+    assert L.sp_layout_make(1024, 1024, 1024, 1, 1, 1, 0, ctypes.byref(lay), ctypes.byref(n)) == 0
+    x_off = lay.origin - lay.gz * lay.pz - lay.gy * lay.py
+    assert (lay.origin * 8) % 128 == 0 and (lay.py * 8) % 128 == 0
+    assert x_off >= lay.gx and x_off + lay.nx + lay.gx <= lay.py
+    assert n.value == lay.pz * (1024 + 2)
+    # fp32: 128-byte aligned rows as well
+    assert L.sp_layout_make(33, 18, 20, 1, 1, 4, 1, ctypes.byref(lay), ctypes.byref(n)) == 0
+    assert (lay.origin * 4) % 128 == 0 and (lay.py * 4) % 16 == 0
+    # GridError on bad extents (R/grid.py:36-41)
+    assert L.sp_layout_make(0, 4, 4, 1, 1, 1, 0, ctypes.byref(lay), ctypes.byref(n)) == 1
+    assert b"interior extents" in L.sp_last_error()
+
+
+def test_griddims_mirror(sp):
+    d = sp.GridDims(4, 5, 6, ghost=2)
+    assert d.shape == (6, 5, 4) and d.alloc_shape == (10, 9, 8)
+    with pytest.raises(sp.GridError):
+        sp.GridDims(0, 4, 4)
+    with pytest.raises(sp.GridError):
+        sp.GridDims(4, 4, 4, ghost=0)
+    with pytest.raises(sp.GridError):
+        sp.FillPattern("nope")
+
+
+def test_pipeline_config_mirror(sp):
+    cfg = sp.PipelineConfig(teams=2, team_size=4, updates_per_thread=2)
+    assert cfg.levels_per_sweep == 16 and cfg.n_threads == 8
+    for bad in [dict(teams=0), dict(min_dist=0), dict(max_dist=0), dict(sync="x"),
+                dict(storage="x"), dict(depth=9)]:
+        with pytest.raises(ValueError):
+            sp.PipelineConfig(**bad)
+    assert sp.default_block_size(sp.GridDims(48, 48, 48), sp.PipelineConfig()) == (48, 16, 16)
+
+
+def test_domains_to_passes(sp):
+    from paper_0912_4506_b200.pipeline import domains_to_passes
+    # rank 1 of 4, h=4, z-slab: z ranges (-3,19),(-2,18),(-1,17),(0,16)
+    doms = [((-3, 0, 0), (19, 8, 8)), ((-2, 0, 0), (18, 8, 8)), ((-1, 0, 0), (17, 8, 8)),
+            ((0, 0, 0), (16, 8, 8))]
+    assert domains_to_passes(doms, 4, 4) == [(4, (0, 0, 0), (16, 8, 8), (1, 0, 0), (1, 0, 0))]
+    assert domains_to_passes(doms, 4, 3) == [(3, (-1, 0, 0), (17, 8, 8), (1, 0, 0), (1, 0, 0)),
+                                             (1, (0, 0, 0), (16, 8, 8), (1, 0, 0), (1, 0, 0))]
+    plain = [((0, 0, 0), (8, 8, 8))] * 5
+    assert domains_to_passes(plain, 5, 2) == [(2, (0, 0, 0), (8, 8, 8), (0, 0, 0), (0, 0, 0))] * 2 + \
+        [(1, (0, 0, 0), (8, 8, 8), (0, 0, 0), (0, 0, 0))]
+    with pytest.raises(sp.ScheduleError):
+        domains_to_passes([((0, 0, 0), (8, 8, 8)), ((-1, 0, 0), (8, 8, 8))], 2, 2)
+
+
+def test_decomposition_geometry(sp):
+    from paper_0912_4506_b200.decomp import _split, face_flags, level_domains_for_rank
+    assert _split(10, 3) == [(0, 4), (4, 7), (7, 10)]
+    d = sp.decompose(sp.GridDims(16, 16, 64), 4, (1, 1, 4), 4)
+    assert d.ranges(1) == ((16, 32), (0, 16), (0, 16))
+    assert level_domains_for_rank(d, 1, 4) == [((-3, 0, 0), (19, 16, 16)), ((-2, 0, 0), (18, 16, 16)),
+                                               ((-1, 0, 0), (17, 16, 16)), ((0, 0, 0), (16, 16, 16))]
+    assert face_flags(d, 0) == ((0, 0, 0), (1, 0, 0))
+    assert face_flags(d, 3) == ((1, 0, 0), (0, 0, 0))
+    with pytest.raises(sp.DecompositionError):
+        sp.decompose(sp.GridDims(16, 16, 16), 3, (1, 1, 2), 1)
+    with pytest.raises(sp.DecompositionError):
+        sp.decompose(sp.GridDims(16, 16, 6), 2, (1, 1, 2), 4)   # 3 cells per rank < h
+
+
+def test_plane_spans_are_contiguous_planes(sp):
+    import torch
+    from paper_0912_4506_b200.decomp import plane_spans
+    L = sp._native.load_library()
+    lay = sp._native.Layout()
+    n = ctypes.c_int64()
+    L.sp_layout_make(5, 4, 10, 1, 1, 3, 0, ctypes.byref(lay), ctypes.byref(n))
+    buf = torch.arange(n.value, dtype=torch.float64)
+    s_lo, s_hi, r_lo, r_hi = plane_spans(buf, lay, 3)
+    assert s_lo.numel() == 3 * lay.pz
+    assert int(s_lo[0]) == 3 * lay.pz                 # plane z=0 follows 3 ghost planes
+    assert int(r_lo[0]) == 0                          # planes -3..-1
+    assert int(s_hi[0]) == (3 + 10 - 3) * lay.pz
+    assert int(r_hi[0]) == (3 + 10) * lay.pz
+
+
+def test_stencil_point_and_compare(sp):
+    assert sp.stencil_point(1.0, 2.0, 3.0, 4.0, 0.0, 5.0) == 15.0 / 6.0
+    a = np.random.default_rng(0).random((4, 4, 4))
+    assert sp.compare(a, a.copy()).bitwise
+    assert sp.REL_TOL == 1e-13
+
+
+def test_no_cpu_fallback(sp, monkeypatch):
+    import torch
+    monkeypatch.setattr(torch.cuda, "is_available", lambda: False)
+    with pytest.raises(sp.NativeUnavailable):
+        sp.TwoGrid(sp.GridDims(4, 4, 4), sp.FillPattern.random(0))
+
+
+def test_product_never_imports_oracle():
+    """The checker stays test infrastructure: no product file imports or loads it."""
+    pkg = os.path.join(ROOT, "paper_0912_4506_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", txt, flags=re.M), f
+                assert "libjacobi_oracle" not in txt, f
