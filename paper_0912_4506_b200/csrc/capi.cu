@@ -14,6 +14,10 @@
 #include <mutex>
 #include <string>
 
+#ifndef SP_L2_PROMO
+#define SP_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -91,10 +95,19 @@ int check_layout(const sp_layout* L, int dtype) {
 // Kernel variants: CTA shape (warps BY x rows-per-thread PY; footprint is
 // 64 x BY*PY) and z-queue depth (2 = shift by moves, 3 = rotating registers).
 struct Variant {
-    int by, py, slots;
+    int by, py, slots, minb, ring;   // warps, rows/thread, z-queue slots, CTAs/SM, TMA ring cap
 };
-constexpr Variant kVariants[] = {{16, 2, 2}, {16, 2, 3}, {8, 4, 2}, {8, 4, 3}, {8, 8, 2}, {16, 4, 2}};
-constexpr int kNumVariants = 6;
+constexpr Variant kVariants[] = {
+    {16, 2, 2, 1, 8},  // 0: fallback for every depth
+    {16, 2, 3, 1, 8},  // 1: fp64 T=2 default
+    {8, 4, 2, 1, 8},   // 2: fp64 T=4 default, fp32 T>4
+    {8, 4, 3, 1, 8},   // 3: fp64 T=3 default
+    {8, 8, 2, 1, 8},   // 4: fp32 T=3..4 default (64x64 footprint)
+    {16, 2, 3, 1, 6},  // 5: T=1 default (shallower ring streams better)
+    {16, 2, 1, 1, 8},  // 6: v[p-1] re-read from shared memory (16 warps)
+    {8, 4, 1, 1, 8},   // 7: same, 8 warps
+};
+constexpr int kNumVariants = 8;
 int g_variant_override = -1;
 
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
@@ -102,16 +115,14 @@ int g_variant_override = -1;
 template <typename R, int T, int V>
 constexpr bool compiled() {
     if (V == 0) return true;
+    if (T == 1) return V == 5 || V == 1;
     if (sizeof(R) == 8) {
-        if (T == 1) return V == 1;
-        if (T == 2) return V == 1 || V == 3 || V == 4;
-        if (T == 3) return V == 2 || V == 3;
-        if (T == 4) return V == 2 || V == 3;
+        if (T == 2) return V == 1 || V == 3 || V == 4 || V >= 6;
+        if (T <= 4) return V == 2 || V == 3 || V >= 6;
         return false;
     }
-    if (T == 1) return V == 1;
-    if (T == 2) return V == 1 || V == 3 || V == 4;
-    if (T <= 4) return V == 2 || V == 3 || V == 4;
+    if (T == 2) return V == 1 || V == 3 || V == 4 || V >= 6;
+    if (T <= 4) return V == 2 || V == 3 || V == 4 || V >= 6;
     return V == 2;
 }
 
@@ -119,14 +130,14 @@ constexpr bool compiled() {
 // profiles/tuning_r01.md): fp64 T=2 16x2/3, T=3 8x4/3, T=4 8x4/2; fp32 T<=2
 // 16x2, T=3..4 8x8/2, deeper 8x4/2.
 int default_variant(int dtype, int T) {
+    if (T == 1) return dtype == SP_F64 ? 5 : 1;
     if (dtype == SP_F64) {
-        if (T == 1) return 1;
         if (T == 2) return 1;
         if (T == 3) return 3;
         if (T == 4) return 2;
         return 0;
     }
-    if (T <= 2) return T == 1 ? 1 : 0;
+    if (T == 2) return 0;
     if (T <= 4) return 4;
     return 2;
 }
@@ -135,17 +146,20 @@ int default_variant(int dtype, int T) {
 bool variant_fits(int dtype, int T, int v) {
     const int es = elem_size(dtype);
     const int wy = kVariants[v].by * kVariants[v].py;
-    const int plane = sp::WX * wy * es, budget = 232448 - 256, nl = T > 1 ? T - 1 : 0;
+    const int minb = kVariants[v].minb;
+    const int plane = sp::WX * wy * es, nl = T > 1 ? T - 1 : 0;
+    const int budget = (minb == 1 ? 232448 : 233472 / minb - 1024) - 256;
     const int nbuf = (2 * nl + 3) * plane <= budget ? 2 : 1;
     int ring = budget / plane - nbuf * nl;
-    if (ring > 8) ring = 8;
-    return ring >= 3 && wy - 2 * T >= 1;
+    if (ring > kVariants[v].ring) ring = kVariants[v].ring;
+    const bool smemq = kVariants[v].slots == 1;
+    return ring >= (smemq ? 4 : 3) && wy - 2 * T >= 1 && (!smemq || nbuf == 2);
 }
 
 template <typename R, int T, int V>
 constexpr bool usable() {
     constexpr Variant v = kVariants[V];
-    return compiled<R, T, V>() && sp::Plan<R, T, v.by, v.py, v.slots>::FITS;
+    return compiled<R, T, V>() && sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>::FITS;
 }
 
 template <typename R, int T>
@@ -156,7 +170,9 @@ bool is_usable(int v) {
         case 2: return usable<R, T, 2>();
         case 3: return usable<R, T, 3>();
         case 4: return usable<R, T, 4>();
-        default: return usable<R, T, 5>();
+        case 5: return usable<R, T, 5>();
+        case 6: return usable<R, T, 6>();
+        default: return usable<R, T, 7>();
     }
 }
 
@@ -188,8 +204,8 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
     } else {
         constexpr Variant v = kVariants[V];
-        using Pl = sp::Plan<R, T, v.by, v.py, v.slots>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots>;
+        using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
+        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
         const size_t smem = Pl::SMEM;
         static bool attr_set = false;  // per instantiation
         if (!attr_set) {
@@ -207,7 +223,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         CUresult r = enc(&map, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                          3, const_cast<void*>(src), gdim, gstride, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                         SP_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
         kern<<<grid, Pl::NT, smem, stream>>>(map, a);
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -226,7 +242,9 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 2: return launch_tb_t<R, T, 2>(src, L, a, grid, s);
         case 3: return launch_tb_t<R, T, 3>(src, L, a, grid, s);
         case 4: return launch_tb_t<R, T, 4>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 5>(src, L, a, grid, s);
+        case 5: return launch_tb_t<R, T, 5>(src, L, a, grid, s);
+        case 6: return launch_tb_t<R, T, 6>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 7>(src, L, a, grid, s);
     }
 }
 
@@ -365,7 +383,7 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
     a.gz = (int)L->gz;
     const int64_t nzb = out_hi[0] - out_lo[0];
     const int64_t tiles = (int64_t)a.ntx * a.nty;
-    const int slots = di.sms;
+    const int slots = di.sms * kVariants[variant].minb;
     // z-chunking: minimise waves * (chunk + 2T) -- the wave-quantised cost of
     // every unit streaming chunk+2T planes.
     int64_t best_n = 1;

@@ -126,40 +126,45 @@ __device__ __forceinline__ Unit decode_unit(const TBArgs& a, int u) {
 // Footprint x origin: x0 - T moved down to a 16-byte boundary of the row
 // (TMA box starts must be 16-byte aligned); the host sizes ox so the shifted
 // footprint still covers [x0 - T, x0 + ox + T).
+template <typename R>
 __device__ __forceinline__ int footprint_x(const TBArgs& a, int x0, int T) {
-    const int A = a.align;                       // elements per 16 bytes
-    int r = (x0 - T + a.x_off) % A;
-    if (r < 0) r += A;
-    return x0 - T - r;
+    constexpr int A = 16 / (int)sizeof(R);       // elements per 16 bytes (power of two)
+    return x0 - T - ((x0 - T + a.x_off) & (A - 1));
 }
 
 // Shared-memory plan per instantiation: a RING-deep TMA ring of level-0
 // planes plus, for levels 1..T-1, one plane each -- double-buffered when it
 // fits (one barrier per step), single-buffered otherwise (two barriers).
-template <typename R, int T, int BY, int PY, int SLOTS = 3>
+template <typename R, int T, int BY, int PY, int SLOTS = 3, int MINB = 1, int RCAP = 8>
 struct Plan {
+    // SLOTS == 1 keeps only v[p] in registers; v[p-1] is re-read from the
+    // double-buffered level plane (and ring slot k-2) just before it is
+    // overwritten, so it needs full planes, double buffering and a ring >= 4.
     static_assert(T * PY <= 64 && T * PX <= 32, "domain bitmasks too narrow");
     static constexpr int WY = BY * PY;
     static constexpr int NT = 32 * BY;
     static constexpr int PLANE = WX * WY;
     static constexpr int PLANE_BYTES = PLANE * (int)sizeof(R);
-    static constexpr int BUDGET = 232448 - 256;             // opt-in smem per CTA, minus barriers
+    // opt-in smem per CTA (MINB CTAs share the SM's 228 KB), minus barriers
+    static constexpr int BUDGET = (MINB == 1 ? 232448 : 233472 / MINB - 1024) - 256;
     static constexpr int NL = (T > 1) ? (T - 1) : 0;        // stored level planes
     static constexpr bool DB = (2 * NL + 3) * PLANE_BYTES <= BUDGET;
     static constexpr int NBUF = DB ? 2 : 1;
     static constexpr int RING_FIT = BUDGET / PLANE_BYTES - NBUF * NL;
-    static constexpr int RING = RING_FIT > 8 ? 8 : RING_FIT;
-    static constexpr bool FITS = RING >= 3 && WY - 2 * T >= 1;
+    static constexpr int RING = RING_FIT > RCAP ? RCAP : RING_FIT;
+    static constexpr int MIN_RING = SLOTS == 1 ? 4 : 3;
+    static constexpr bool FITS = RING >= MIN_RING && WY - 2 * T >= 1 && (SLOTS != 1 || DB);
     static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + RING * 8;
 };
 
-template <typename R, int T, int BY, int PY, int SLOTS>
-__global__ void __launch_bounds__(32 * BY, 1)
+template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP>
+__global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
-    static_assert(SLOTS == 2 || SLOTS == 3, "z-queue slots");
+    static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
+    constexpr int QN = SLOTS == 1 ? 2 : SLOTS;   // register slots per level
     using A = Arith<R>;
     using V2 = typename A::V2;
-    using P = Plan<R, T, BY, PY, SLOTS>;
+    using P = Plan<R, T, BY, PY, SLOTS, MINB, RCAP>;
     constexpr int WY = P::WY;
     constexpr int PLANE = P::PLANE;
     constexpr int RING_N = P::RING;
@@ -184,24 +189,30 @@ __global__ void __launch_bounds__(32 * BY, 1)
     __syncthreads();
 
     // Producer cursor (thread 0 only): walks the same (unit, step) sequence.
-    int pu = blockIdx.x, ps = 0;
-    Unit pw;
-    if (pu < a.units) pw = decode_unit(a, pu);
+    // TMA coordinates (c0, c1, c2) of the next plane and the unit's last c2.
+    int pu = blockIdx.x, pc0 = 0, pc1 = 0, pc2 = 0, pc2_end = 0;
+    auto producer_unit = [&]() {
+        if (pu >= a.units) return;
+        const Unit pw = decode_unit(a, pu);
+        pc0 = footprint_x<R>(a, pw.x0, T) + a.x_off;
+        pc1 = pw.y0 - T + a.gy;
+        pc2 = pw.zc0 - T + a.gz;
+        pc2_end = pw.zc1 + T + a.gz;
+    };
+    producer_unit();
     auto produce = [&](int slot) {
         if (pu >= a.units) return;
-        int q = pw.zc0 - T + ps;
         mbar_expect_tx(&full[slot], kPlaneBytes);
-        tma_load_3d(ring + slot * PLANE, &tmap, &full[slot], footprint_x(a, pw.x0, T) + a.x_off,
-                    pw.y0 - T + a.gy, q + a.gz);
-        if (++ps == (pw.zc1 - pw.zc0) + 2 * T) {
-            ps = 0;
+        tma_load_3d(ring + slot * PLANE, &tmap, &full[slot], pc0, pc1, pc2);
+        if (++pc2 == pc2_end) {
             pu += gridDim.x;
-            if (pu < a.units) pw = decode_unit(a, pu);
+            producer_unit();
         }
     };
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-        for (int i = 0; i < RING_N - 1; ++i) produce(i);   // slot RING-1 is filled after step 0
+        // the slot released after step k is k-1 (k-2 with SLOTS == 1): prime the rest
+        for (int i = 0; i < RING_N - (SLOTS == 1 ? 2 : 1); ++i) produce(i);
     }
 
     const R sixth = A::sixth();
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
 
     for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
         const Unit w = decode_unit(a, u);
-        const int fx = footprint_x(a, w.x0, T), fy = w.y0 - T;
+        const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T;
         const int nsteps = (w.zc1 - w.zc0) + 2 * T;
 
         // Per-level x/y domain of this thread's columns: x bits (PX per level)
@@ -262,9 +273,11 @@ __global__ void __launch_bounds__(32 * BY, 1)
         // unrolled by 3, so there are no register moves.  SLOTS == 2: Q[0] =
         // v[p-1], Q[1] = v[p], the new plane lives in a transient and the
         // queue shifts by moves (fewer live registers, more instructions).
-        R Q[SLOTS][T][PY][PX];
+        // SLOTS == 1: Q[f] = v[p] and Q[f^1] = v[p+1] (new), steps unrolled by 2;
+        // v[p-1] comes back from shared memory.
+        R Q[QN][T][PY][PX];
 #pragma unroll
-        for (int f = 0; f < SLOTS; ++f)
+        for (int f = 0; f < QN; ++f)
 #pragma unroll
             for (int t = 0; t < T; ++t)
 #pragma unroll
@@ -277,12 +290,14 @@ __global__ void __launch_bounds__(32 * BY, 1)
         // straight-line; otherwise cells outside D_t keep their previous-level
         // value (Dirichlet walls, rank faces) through a per-cell select.
         auto step = [&](auto phase, auto fast, int st) {
-            constexpr int F0 = SLOTS == 3 ? decltype(phase)::value : 0;    // v[p-1]
-            constexpr int F1 = SLOTS == 3 ? (F0 + 1) % 3 : 1;              // v[p]
-            constexpr int F2 = SLOTS == 3 ? (F0 + 2) % 3 : 0;              // v[p+1] (3 slots)
+            constexpr int PH = decltype(phase)::value;
+            constexpr int F0 = SLOTS == 3 ? PH : 0;                                   // v[p-1]
+            constexpr int F1 = SLOTS == 3 ? (PH + 1) % 3 : (SLOTS == 1 ? PH : 1);    // v[p]
+            constexpr int F2 = SLOTS == 3 ? (PH + 2) % 3 : (SLOTS == 1 ? PH ^ 1 : 0); // v[p+1]
             constexpr bool FAST = decltype(fast)::value;
             const int slot = gstep % RING_N;
             const int pslot = (gstep + RING_N - 1) % RING_N;
+            const int pslot2 = (gstep + RING_N - 2) % RING_N;
             const int cur = P::DB ? (int)(gstep & 1u) : 0;
             const int prv = P::DB ? cur ^ 1 : 0;
             const int q = w.zc0 - T + st;
@@ -316,11 +331,22 @@ __global__ void __launch_bounds__(32 * BY, 1)
 
             mbar_wait(&full[slot], (gstep / RING_N) & 1);
             // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
-            R Nt[SLOTS == 3 ? 1 : T][PY][PX];
+            R Nt[SLOTS == 2 ? T : 1][PY][PX];
             auto newv = [&](int t) -> R(&)[PY][PX] {
-                if constexpr (SLOTS == 3) return Q[F2][t];
+                if constexpr (SLOTS != 2) return Q[F2][t];
                 else return Nt[t];
             };
+            // SLOTS == 1: v[p-1] of level t-1, re-read from shared memory
+            R mv[SLOTS == 1 ? PY : 1][PX];
+            if constexpr (SLOTS == 1) {
+                const R* L2 = ring + pslot2 * PLANE;   // level 0, plane q-2
+#pragma unroll
+                for (int j = 0; j < PY; ++j) {
+                    V2 r = *reinterpret_cast<const V2*>(L2 + (cy + j) * WX + cx);
+                    mv[j][0] = r.x;
+                    mv[j][1] = r.y;
+                }
+            }
             {
                 const R* L0 = ring + slot * PLANE;
                 R(&n0)[PY][PX] = newv(0);
@@ -335,7 +361,10 @@ __global__ void __launch_bounds__(32 * BY, 1)
 #pragma unroll
             for (int t = 1; t <= T; ++t) {
                 if constexpr (P::DB) xy_sums(t);
-                const R(&mm)[PY][PX] = Q[F0][t - 1];
+                const R(&mm)[PY][PX] = *([&]() -> const R(*)[PY][PX] {
+                    if constexpr (SLOTS == 1) return &mv;
+                    else return &Q[F0][t - 1];
+                }());
                 const R(&cc)[PY][PX] = Q[F1][t - 1];
                 const R(&nn)[PY][PX] = newv(t - 1);
                 R(&dst)[PY][PX] = (t < T) ? newv(t < T ? t : 0) : out;
@@ -363,10 +392,24 @@ __global__ void __launch_bounds__(32 * BY, 1)
                     }
                 if (t < T) {
                     R* Pl = lvl + ((t - 1) * P::NBUF + cur) * PLANE;
-                    *reinterpret_cast<V2*>(Pl + cy * WX + cx) = V2{dst[0][0], dst[0][1]};
-                    if (PY > 1)
-                        *reinterpret_cast<V2*>(Pl + (cy + PY - 1) * WX + cx) =
-                            V2{dst[PY - 1][0], dst[PY - 1][1]};
+                    if constexpr (SLOTS == 1) {
+                        // this buffer still holds level t at plane q-t-1 = v[p-1]
+                        // of level t+1: read it back, then store the full new plane
+#pragma unroll
+                        for (int j = 0; j < PY; ++j) {
+                            V2 r = *reinterpret_cast<const V2*>(Pl + (cy + j) * WX + cx);
+                            mv[j][0] = r.x;
+                            mv[j][1] = r.y;
+                        }
+#pragma unroll
+                        for (int j = 0; j < PY; ++j)
+                            *reinterpret_cast<V2*>(Pl + (cy + j) * WX + cx) = V2{dst[j][0], dst[j][1]};
+                    } else {
+                        *reinterpret_cast<V2*>(Pl + cy * WX + cx) = V2{dst[0][0], dst[0][1]};
+                        if (PY > 1)
+                            *reinterpret_cast<V2*>(Pl + (cy + PY - 1) * WX + cx) =
+                                V2{dst[PY - 1][0], dst[PY - 1][1]};
+                    }
                 }
             }
             // level T: write the finished plane (once the pipeline is full)
@@ -386,10 +429,10 @@ __global__ void __launch_bounds__(32 * BY, 1)
                 }
             }
             __syncthreads();
-            // ring slot pslot (read for level 1's sums this step) is free now
+            // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
             if (threadIdx.x == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                produce(pslot);
+                produce(SLOTS == 1 ? pslot2 : pslot);
             }
             ++gstep;
         };
@@ -405,7 +448,12 @@ __global__ void __launch_bounds__(32 * BY, 1)
             else step(phase, std::false_type{}, st);
         };
 
-        if constexpr (SLOTS == 3) {
+        if constexpr (SLOTS == 1) {
+            for (int st = 0; st < nsteps; st += 2) {
+                run(std::integral_constant<int, 0>{}, st);
+                if (st + 1 < nsteps) run(std::integral_constant<int, 1>{}, st + 1);
+            }
+        } else if constexpr (SLOTS == 3) {
             for (int st = 0; st < nsteps; st += 3) {
                 run(std::integral_constant<int, 0>{}, st);
                 if (st + 1 < nsteps) run(std::integral_constant<int, 1>{}, st + 1);
