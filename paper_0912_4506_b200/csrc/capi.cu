@@ -23,6 +23,7 @@ namespace {
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 int g_chunks = 0;
+int g_use_k1 = 0;   // 1: single-level sweeps use the L1-streaming K1 kernel instead of K2(T=1)
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -278,6 +279,8 @@ int sp_set_tuning(int variant, int chunks) {
     int prev = (g_variant_override + 1) * 1000 + g_chunks;
     g_variant_override = variant - 1;   // 0 = automatic, k = variant k-1
     g_chunks = chunks;
+    g_use_k1 = variant < 0 ? 1 : 0;   // variant -1: K1 for single-level sweeps
+    if (variant < 0) g_variant_override = -1;
     return prev;
 }
 
@@ -417,7 +420,47 @@ int sp_sweep_tb(const void* src, void* dst, int dtype, const sp_layout* L, int T
 
 int sp_update_region(const void* src, void* dst, int dtype, const sp_layout* L,
                      const int64_t lo[3], const int64_t hi[3], void* stream) {
-    return sp_sweep_tb(src, dst, dtype, L, 1, lo, hi, nullptr, nullptr, stream);
+    if (!g_use_k1) return sp_sweep_tb(src, dst, dtype, L, 1, lo, hi, nullptr, nullptr, stream);
+    int rc = check_layout(L, dtype);
+    if (rc) return rc;
+    if (!src || !dst || !lo || !hi) return fail(SP_ERR_ARG, "null argument");
+    if (src == dst) return fail(SP_ERR_ARG, "src and dst must be distinct arrays");
+    const int64_t n[3] = {L->nz, L->ny, L->nx};
+    const int64_t g[3] = {L->gz, L->gy, L->gx};
+    for (int d = 0; d < 3; ++d) {
+        if (lo[d] > hi[d]) return fail(SP_ERR_GRID, "malformed region");
+        if (lo[d] - 1 < -g[d] || hi[d] + 1 > n[d] + g[d])
+            return fail(SP_ERR_GRID, "region escapes allocation (axis %d)", d);
+    }
+    for (int d = 0; d < 3; ++d)
+        if (lo[d] == hi[d]) return SP_OK;
+    DevInfo di;
+    rc = dev_info(&di);
+    if (rc) return rc;
+    sp::K1Args a;
+    a.src = src;
+    a.dst = dst;
+    a.py = L->py; a.pz = L->pz; a.origin = L->origin;
+    for (int d = 0; d < 3; ++d) { a.lo[d] = (int)lo[d]; a.hi[d] = (int)hi[d]; }
+    // x pairs start at even x: interior x = 0 is 128-byte aligned (sp_layout_make)
+    a.x0 = (int)(lo[2] - ((lo[2] % 2) + 2) % 2);
+    const int64_t npairs = (hi[2] - a.x0 + 1) / 2;
+    const int64_t nbx = (npairs + 31) / 32, nby = (hi[1] - lo[1] + 7) / 8;
+    const int64_t nzb = hi[0] - lo[0];
+    // enough z-chunks for ~8 CTAs (64 warps) per SM, long enough to amortise the queue fill
+    int64_t want = (int64_t)di.sms * 8;
+    int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(nzb, (want + nbx * nby - 1) / (nbx * nby)));
+    a.zchunk = (int)((nzb + chunks - 1) / chunks);
+    chunks = (nzb + a.zchunk - 1) / a.zchunk;
+    if (nbx > INT32_MAX || nby > 65535 || chunks > 65535) return fail(SP_ERR_SCHEDULE, "grid too large");
+    dim3 grid((unsigned)nbx, (unsigned)nby, (unsigned)chunks), block(32, 8);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == SP_F64) sp::k1_kernel<double><<<grid, block, 0, s>>>(a);
+    else sp::k1_kernel<float><<<grid, block, 0, s>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "k1_kernel launch");
+    return SP_OK;
 }
 
 int sp_run_sweeps(void* a, void* b, int dtype, const sp_layout* L, int64_t levels, int T,
@@ -432,7 +475,8 @@ int sp_run_sweeps(void* a, void* b, int dtype, const sp_layout* L, int64_t level
         int t = (int)std::min<int64_t>(T, levels);
         void* cur = act ? b : a;
         void* oth = act ? a : b;
-        int rc = sp_sweep_tb(cur, oth, dtype, L, t, lo, hi, nullptr, nullptr, stream);
+        int rc = t == 1 ? sp_update_region(cur, oth, dtype, L, lo, hi, stream)
+                        : sp_sweep_tb(cur, oth, dtype, L, t, lo, hi, nullptr, nullptr, stream);
         if (rc) return rc;
         act ^= 1;
         levels -= t;

@@ -465,6 +465,60 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     }
 }
 
+// ---- K1: single-level streaming sweep ---------------------------------------
+//
+// One level over a box (update_region, R/kernel.py:37-40).  A thread owns a
+// 16-byte x pair (fp64; 8 bytes fp32) of one row and marches it through a
+// z-chunk with the column's z-neighbours in a register queue (m, c, n);
+// x/y neighbours are read through L1 (__ldg), where the 8 rows a CTA covers
+// and its lane neighbours make them hits.  No shared memory and ~40
+// registers, so 64 warps per SM hide the DRAM latency; loads/stores are
+// 16-byte and coalesced along x.
+struct K1Args {
+    const void* src;
+    void* dst;
+    int64_t py, pz, origin;
+    int lo[3], hi[3];
+    int x0;                    // first x of the pair grid (lo_x rounded down to a 16-byte pair)
+    int zchunk;
+};
+
+template <typename R>
+__global__ void __launch_bounds__(256) k1_kernel(const K1Args a) {
+    using A = Arith<R>;
+    using V2 = typename A::V2;
+    const R* __restrict__ src = reinterpret_cast<const R*>(a.src) + a.origin;
+    R* __restrict__ dst = reinterpret_cast<R*>(a.dst) + a.origin;
+    const int x = a.x0 + 2 * (blockIdx.x * 32 + threadIdx.x);
+    const int y = a.lo[1] + blockIdx.y * 8 + threadIdx.y;
+    const int z0 = a.lo[0] + blockIdx.z * a.zchunk;
+    const int z1 = min(z0 + a.zchunk, a.hi[0]);
+    if (x >= a.hi[2] || y >= a.hi[1] || z0 >= z1) return;
+    const bool w0 = x >= a.lo[2], w1 = x + 1 < a.hi[2];
+    const int64_t col = (int64_t)y * a.py + x;
+    const R* p = src + (int64_t)z0 * a.pz + col;
+    R* d = dst + (int64_t)z0 * a.pz + col;
+    const R sixth = A::sixth();
+    V2 m = __ldg(reinterpret_cast<const V2*>(p - a.pz));
+    V2 c = __ldg(reinterpret_cast<const V2*>(p));
+    for (int z = z0; z < z1; ++z, p += a.pz, d += a.pz) {
+        const V2 n = __ldg(reinterpret_cast<const V2*>(p + a.pz));
+        const R xm = __ldg(p - 1), xp = __ldg(p + 2);
+        const V2 ym = __ldg(reinterpret_cast<const V2*>(p - a.py));
+        const V2 yp = __ldg(reinterpret_cast<const V2*>(p + a.py));
+        V2 o;
+        o.x = A::mul(A::add(A::add(A::add(xm, c.y), A::add(ym.x, yp.x)), A::add(m.x, n.x)), sixth);
+        o.y = A::mul(A::add(A::add(A::add(c.x, xp), A::add(ym.y, yp.y)), A::add(m.y, n.y)), sixth);
+        if (w0 && w1) __stcs(reinterpret_cast<V2*>(d), o);
+        else {
+            if (w0) __stcs(d, o.x);
+            if (w1) __stcs(d + 1, o.y);
+        }
+        m = c;
+        c = n;
+    }
+}
+
 // ---- K3: pattern fill -------------------------------------------------------
 
 struct FillArgs {

@@ -281,6 +281,43 @@ class _on:
         self._ctx.__exit__(*a)
 
 
+class ArrayPattern:
+    """Duck-typed pattern over a host field holding the ghosted box
+    (z, y, x) of ``dims`` -- e.g. the array ``load_field`` returns -- so a
+    dumped grid can be re-created on the device: ``TwoGrid(dims, ArrayPattern(...))``."""
+
+    def __init__(self, field: np.ndarray, ghost: int):
+        self.field = np.asarray(field)
+        self.ghost = ghost
+
+    def evaluate(self, lo, hi) -> np.ndarray:
+        g = self.ghost
+        sl = tuple(slice(l + g, h + g) for l, h in zip(lo, hi))
+        return self.field[sl]
+
+
+def dump_field(grid, fh) -> None:
+    """Text dump compatible with the reference (R/grid.py:280-289): header
+    ``nx ny nz ghost`` then the ghosted box, x fastest, one %.17g value per line."""
+    d = grid.dims
+    full = grid.full_view()
+    if full.shape != d.alloc_shape:
+        raise GridError("dump needs a grid with the same ghost depth on every axis")
+    fh.write(f"{d.nx} {d.ny} {d.nz} {d.ghost}\n")
+    fh.write("".join("%.17g\n" % v for v in full.astype(np.float64).ravel()))
+
+
+def load_field(fh) -> tuple[GridDims, np.ndarray]:
+    """Parse a dump (R/grid.py:293-300) into (dims, ghosted host field)."""
+    header = fh.readline().split()
+    nx, ny, nz, ghost = (int(t) for t in header)
+    dims = GridDims(nx, ny, nz, ghost)
+    flat = np.array([float(line) for line in fh], dtype=np.float64)
+    if flat.size != int(np.prod(dims.alloc_shape)):
+        raise GridError("dump payload does not match header extents")
+    return dims, flat.reshape(dims.alloc_shape)
+
+
 def allocate(dims: GridDims, mode: str, pattern, slack: int = 0, **kw):
     """Allocate and initialise a device grid (R/grid.py:217-223); two-grid only."""
     if mode == "twogrid":

@@ -273,3 +273,44 @@ def test_every_cta_shape(sp, O, shape_id, dtype):
             assert bitwise(g.interior(), ref.interior()), (shape_id, shape, depth)
     finally:
         lib.sp_set_tuning(0, 0)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_k1_streaming_kernel(sp, O, dtype):
+    """K1 (L1-streaming, no shared memory) for single-level sweeps and sub-boxes."""
+    lib = sp._native.lib()
+    lib.sp_set_tuning(-1, 0)
+    try:
+        for shape, levels in [((9, 7, 5), 4), ((33, 70, 129), 3), ((1, 1, 1), 2), ((64, 24, 56), 5)]:
+            faces = (0.3, -1.0, 2.0, 0.0, 1.0, -0.5)
+            g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, faces, seed=3),
+                           dtype=dtype)
+            sp.sweeps(g, levels, depth=1)
+            ref = oracle_run(O, shape, "random", 3, faces, levels, dtype=dtype)
+            assert bitwise(g.interior(), ref.interior()), shape
+        shape = (9, 10, 11)
+        g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.random(5), dtype=dtype)
+        ref = O.CGrid(shape, O.BoxPattern("random", seed=5), dtype=dtype)
+        for lo, hi in [((2, 3, 1), (7, 9, 5)), ((0, 0, 3), (9, 10, 11))]:
+            sp.update_block(g, lo, hi, level=1)
+            ref.update_region(lo, hi, level=1)
+            assert bitwise(g.other.cpu().numpy(), ref.b if ref.active == 0 else ref.a)
+    finally:
+        lib.sp_set_tuning(0, 0)
+
+
+def test_dump_load_round_trip(sp, O):
+    import io
+    shape = (5, 6, 7)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.random(21))
+    sp.sweeps(g, 3, depth=3)
+    buf = io.StringIO()
+    sp.dump_field(g, buf)
+    buf.seek(0)
+    dims, field = sp.load_field(buf)
+    h = sp.TwoGrid(dims, sp.ArrayPattern(field, dims.ghost))
+    assert bitwise(h.full_view(), g.full_view())
+    sp.sweeps(g, 2, depth=2)
+    sp.sweeps(h, 2, depth=1)
+    ref = oracle_run(O, shape, "random", 21, None, 5)
+    assert bitwise(g.interior(), ref.interior()) and bitwise(h.interior(), ref.interior())

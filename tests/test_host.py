@@ -128,3 +128,23 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", txt, flags=re.M), f
                 assert "libjacobi_oracle" not in txt, f
+
+
+def test_load_field_reads_reference_dump(sp):
+    """A dump written by the reference itself (R/grid.py:280-289) parses here."""
+    import io
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        from stencilpipe.grid import FillPattern, GridDims, TwoGrid, dump_field
+    except ImportError:
+        pytest.skip("reference package not present")
+    g = TwoGrid(GridDims(3, 4, 5), FillPattern.random(9))
+    buf = io.StringIO()
+    dump_field(g, buf)
+    buf.seek(0)
+    dims, field = sp.load_field(buf)
+    assert (dims.nx, dims.ny, dims.nz, dims.ghost) == (3, 4, 5, 1)
+    assert np.array_equal(field.view(np.uint64), g.current.view(np.uint64))
+    pat = sp.ArrayPattern(field, 1)
+    assert np.array_equal(pat.evaluate((0, 0, 0), (5, 4, 3)), g.interior())
