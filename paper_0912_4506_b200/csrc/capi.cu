@@ -97,18 +97,20 @@ int check_layout(const sp_layout* L, int dtype) {
 // 64 x BY*PY) and z-queue depth (2 = shift by moves, 3 = rotating registers).
 struct Variant {
     int by, py, slots, minb, ring;   // warps, rows/thread, z-queue slots, CTAs/SM, TMA ring cap
+    int rstore;                      // 1: running output pointer (see tb_kernel)
 };
 constexpr Variant kVariants[] = {
-    {16, 2, 2, 1, 8},  // 0: fallback for every depth
-    {16, 2, 3, 1, 8},  // 1: fp64 T=2 default
-    {8, 4, 2, 1, 8},   // 2: fp64 T=4 default, fp32 T>4
-    {8, 4, 3, 1, 8},   // 3: fp64 T=3 default
-    {8, 8, 2, 1, 8},   // 4: fp32 T=3..4 default (64x64 footprint)
-    {16, 2, 3, 1, 6},  // 5: T=1 default (shallower ring streams better)
-    {16, 2, 1, 1, 8},  // 6: v[p-1] re-read from shared memory (16 warps)
-    {8, 4, 1, 1, 8},   // 7: same, 8 warps
+    {16, 2, 2, 1, 8, 0},  // 0: fallback for every depth
+    {16, 2, 3, 1, 8, 0},  // 1: fp64 T=2 default
+    {8, 4, 2, 1, 8, 0},   // 2: fp64 T=4 default, fp32 T>4
+    {8, 4, 3, 1, 8, 0},   // 3: fp64 T=3 default
+    {8, 8, 2, 1, 8, 0},   // 4: fp32 T=3 default (64x64 footprint)
+    {16, 2, 3, 1, 6, 0},  // 5: T=1 default (shallower ring streams better)
+    {16, 2, 1, 1, 8, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
+    {8, 4, 1, 1, 8, 0},   // 7: same, 8 warps
+    {8, 8, 2, 1, 8, 1},   // 8: fp32 T=4 default: 4 with the running output pointer
 };
-constexpr int kNumVariants = 8;
+constexpr int kNumVariants = 9;
 int g_variant_override = -1;
 
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
@@ -116,6 +118,7 @@ int g_variant_override = -1;
 template <typename R, int T, int V>
 constexpr bool compiled() {
     if (V == 0) return true;
+    if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (T == 1) return V == 5 || V == 1;
     if (sizeof(R) == 8) {
         if (T == 2) return V == 1 || V == 3 || V == 4 || V >= 6;
@@ -139,7 +142,8 @@ int default_variant(int dtype, int T) {
         return 0;
     }
     if (T == 2) return 0;
-    if (T <= 4) return 4;
+    if (T == 3) return 4;
+    if (T == 4) return 8;
     return 2;
 }
 
@@ -173,7 +177,8 @@ bool is_usable(int v) {
         case 4: return usable<R, T, 4>();
         case 5: return usable<R, T, 5>();
         case 6: return usable<R, T, 6>();
-        default: return usable<R, T, 7>();
+        case 7: return usable<R, T, 7>();
+        default: return usable<R, T, 8>();
     }
 }
 
@@ -206,7 +211,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
     } else {
         constexpr Variant v = kVariants[V];
         using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
+        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore>;
         const size_t smem = Pl::SMEM;
         static bool attr_set = false;  // per instantiation
         if (!attr_set) {
@@ -245,7 +250,8 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 4: return launch_tb_t<R, T, 4>(src, L, a, grid, s);
         case 5: return launch_tb_t<R, T, 5>(src, L, a, grid, s);
         case 6: return launch_tb_t<R, T, 6>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 7>(src, L, a, grid, s);
+        case 7: return launch_tb_t<R, T, 7>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 8>(src, L, a, grid, s);
     }
 }
 

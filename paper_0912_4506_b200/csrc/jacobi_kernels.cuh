@@ -157,7 +157,7 @@ struct Plan {
     static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + RING * 8;
 };
 
-template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP>
+template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
@@ -264,6 +264,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             wyb |= (gyy >= w.y0 && gyy < min(w.y0 + a.oy, a.ohi[1]) ? 1u : 0u) << j;
         }
         R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
+        const int64_t pz = a.pz, py = a.py;
+        R* dnext = dcol + (int64_t)(w.zc0 - 2 * T) * pz;   // plane q-T of step 0
         // both x cells written and the pair 16-byte aligned (same for every row: py is)
         const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
 
@@ -412,22 +414,28 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     }
                 }
             }
-            // level T: write the finished plane (once the pipeline is full)
+            // level T: write the finished plane (once the pipeline is full).
+            // RSTORE: dnext points at plane q-T of this thread's patch and
+            // advances one plane per step; otherwise the address is formed per
+            // step.  Both are bit-identical -- ptxas schedules them differently
+            // and the tuned variant table picks per (dtype, T).
             if (st >= 2 * T) {
-                R* d = dcol + (int64_t)(q - T) * a.pz;
+                R* d = RSTORE ? dnext : dcol + (int64_t)(q - T) * pz;
                 if (vec_store) {
 #pragma unroll
                     for (int j = 0; j < PY; ++j)
-                        if ((wyb >> j) & 1u) *reinterpret_cast<V2*>(d + j * a.py) = V2{out[j][0], out[j][1]};
+                        if ((wyb >> j) & 1u)
+                            __stcs(reinterpret_cast<V2*>(d + j * py), V2{out[j][0], out[j][1]});
                 } else {
 #pragma unroll
                     for (int j = 0; j < PY; ++j) {
                         const bool row = (wyb >> j) & 1u;
-                        if (row && (wx & 1u)) d[j * a.py] = out[j][0];
-                        if (row && (wx & 2u)) d[j * a.py + 1] = out[j][1];
+                        if (row && (wx & 1u)) __stcs(d + j * py, out[j][0]);
+                        if (row && (wx & 2u)) __stcs(d + j * py + 1, out[j][1]);
                     }
                 }
             }
+            if (RSTORE) dnext += pz;
             __syncthreads();
             // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
             if (threadIdx.x == 0) {
