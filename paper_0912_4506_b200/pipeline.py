@@ -77,6 +77,46 @@ def default_block_size(dims: GridDims, cfg: PipelineConfig) -> tuple[int, int, i
     return (dims.nx, by, bz)
 
 
+def check_schedule(dims: GridDims, cfg: PipelineConfig, level_domains=None) -> None:
+    """The reference's schedule validation (R/pipeline.py:216-243, 187-201).
+
+    The device wavefront does not use blocks, but a configuration the
+    reference would reject is rejected here too, with the same ScheduleError:
+    U larger than the smallest extent, the wrong number of level domains, or
+    block edges that escape a level's domain once shifted by -(tau-1).
+    """
+    from .kernel import block_edges
+    U = cfg.levels_per_sweep
+    shape = dims.shape
+    if U > min(shape):
+        raise ScheduleError(
+            f"U={U} updates per node sweep exceed the smallest interior "
+            f"extent {min(shape)}; degenerate pipeline")
+    if level_domains is None:
+        level_domains = [((0, 0, 0), shape)] * U
+    elif len(level_domains) != U:
+        raise ScheduleError(f"need {U} level domains, got {len(level_domains)}")
+    base_lo, base_hi = level_domains[0]
+    if cfg.block is None:
+        edges = [[base_lo[d], base_hi[d]] for d in range(3)]
+    else:
+        bx, by, bz = cfg.block
+        edges = [[base_lo[d] + e for e in block_edges(base_hi[d] - base_lo[d], b)]
+                 for d, b in zip(range(3), (bz, by, bx))]
+    for tau in range(1, U + 1):
+        shift = -(tau - 1)
+        dom_lo, dom_hi = level_domains[tau - 1]
+        for d in range(3):
+            e = edges[d]
+            m = len(e) - 1
+            if m == 1:
+                continue
+            if e[1] + shift < dom_lo[d] or e[m - 1] + shift > dom_hi[d]:
+                raise ScheduleError(
+                    f"level {tau}: shifted block edges escape domain "
+                    f"(dim {d}, shift {shift}); shrink U or enlarge blocks")
+
+
 def domains_to_passes(level_domains, U: int, depth: int):
     """Split U levels with domains D_1..D_U into device passes.
 
@@ -160,17 +200,12 @@ def run_node_sweeps(grid: TwoGrid, cfg: PipelineConfig, sweeps_: int,
     if cfg.storage != "twogrid":
         raise ValueError("config expects compressed storage but the device grid is two-grid")
     U = cfg.levels_per_sweep
-    if U > min(grid.dims.shape):
-        raise ScheduleError(
-            f"U={U} updates per node sweep exceed the smallest interior "
-            f"extent {min(grid.dims.shape)}; degenerate pipeline")
+    check_schedule(grid.dims, cfg, level_domains)
     depth = cfg.depth or DEFAULT_DEPTH[grid.sp_dtype]
     if level_domains is None:
         for _ in range(sweeps_):
             sweeps(grid, U, depth)
         return
-    if len(level_domains) != U:
-        raise ScheduleError(f"need {U} level domains, got {len(level_domains)}")
     passes = domains_to_passes(level_domains, U, depth)
     for _ in range(sweeps_):
         for T, lo, hi, e_lo, e_hi in passes:

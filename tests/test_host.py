@@ -148,3 +148,32 @@ def test_load_field_reads_reference_dump(sp):
     assert np.array_equal(field.view(np.uint64), g.current.view(np.uint64))
     pat = sp.ArrayPattern(field, 1)
     assert np.array_equal(pat.evaluate((0, 0, 0), (5, 4, 3)), g.interior())
+
+
+def test_schedule_validation_matches_reference(sp):
+    """check_schedule raises exactly where the reference's build_schedule does."""
+    import sys
+    from paper_0912_4506_b200.pipeline import check_schedule
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        from stencilpipe import pipeline as rp
+        from stencilpipe.grid import GridDims as RDims
+    except ImportError:
+        pytest.skip("reference package not present")
+    cases = [((8, 8, 8), dict(teams=1, team_size=1, updates_per_thread=4, block=(8, 2, 2))),
+             ((8, 8, 8), dict(teams=1, team_size=2, updates_per_thread=2, block=(8, 4, 4))),
+             ((24, 24, 24), dict(teams=2, team_size=4, updates_per_thread=2, block=(24, 16, 16))),
+             ((12, 10, 9), dict(teams=1, team_size=1, updates_per_thread=5, block=(12, 3, 3))),
+             ((4, 4, 4), dict(teams=1, team_size=1, updates_per_thread=5)),
+             ((16, 16, 16), dict(teams=1, team_size=2, updates_per_thread=1, block=(16, 1, 1)))]
+    for (nx, ny, nz), kw in cases:
+        ref_err = ours_err = None
+        try:
+            rp.build_schedule(RDims(nx, ny, nz), rp.PipelineConfig(**kw))
+        except rp.ScheduleError:
+            ref_err = True
+        try:
+            check_schedule(sp.GridDims(nx, ny, nz), sp.PipelineConfig(**kw))
+        except sp.ScheduleError:
+            ours_err = True
+        assert ref_err == ours_err, ((nx, ny, nz), kw)
