@@ -1,16 +1,16 @@
-"""z-slab decomposition with depth-h halos (drop-in for R/decomp.py).
+"""Domain decomposition with depth-h halos (drop-in for R/decomp.py).
 
 Geometry (``_split``, ``Decomposition``, ``level_domains_for_rank``) is the
-reference's host logic restated.  The device engine supports layouts
-(1, 1, P): ranks are z-slabs, each keeping x/y ghosts of depth 1 and z
-ghosts of depth h.  A halo exchange moves h padded z-planes to each z
-neighbour; because z is the outermost axis those planes are contiguous, so
-every message is one contiguous copy straight from the grid into the
-neighbour's ghost planes -- no pack/unpack kernel (R/grid.py:247-277 is not
-needed).  ``run_distributed`` keeps the reference's single-call,
-all-ranks-in-one-process contract (R/decomp.py:240-268, ranks as threads of
-one process); ranks are placed round-robin on the visible GPUs and exchange
-by device copies.  The multi-process NCCL engine is ``dist.SlabRunner``.
+reference's host logic restated.  The primary layout is (1, 1, P): ranks
+are z-slabs with x/y ghosts of depth 1 and z ghosts of depth h, and a halo
+exchange moves h padded z-planes -- contiguous, since z is the outermost
+axis -- straight from the grid into the neighbour's ghost planes (no
+pack/unpack kernel, R/grid.py:247-277).  General (px, py, pz) layouts use
+the reference's x -> y -> z extended-slab exchange (R/decomp.py:125-179)
+as strided device copies.  ``run_distributed`` keeps the reference's
+single-call, all-ranks-in-one-process contract (R/decomp.py:240-268); ranks
+are placed round-robin on the visible GPUs.  The multi-process NCCL engine
+(z-slabs) is ``dist.SlabRunner``.
 (R = /root/reference/pkg/src/stencilpipe)
 """
 
@@ -113,13 +113,6 @@ def level_domains_for_rank(decomp: Decomposition, rank: int, h: int):
     return domains
 
 
-def _require_zslab(layout):
-    if tuple(layout[:2]) != (1, 1):
-        raise DecompositionError(
-            f"layout {tuple(layout)}: the device engine decomposes in z only (1, 1, P); "
-            "multi-axis layouts are out of scope (DESIGN.md)")
-
-
 def face_flags(decomp: Decomposition, rank: int):
     """(ext_lo, ext_hi) per array axis: 1 where the face has a neighbour."""
     e_lo = tuple(int(decomp.neighbor(rank, d, high=False) is not None) for d in range(3))
@@ -128,15 +121,17 @@ def face_flags(decomp: Decomposition, rank: int):
 
 
 def local_grid(decomp: Decomposition, rank: int, pattern, dtype=np.float64, device=None) -> TwoGrid:
-    """Rank-local device grid: z ghosts of depth h, x/y ghosts of depth 1."""
-    _require_zslab(decomp.layout)
+    """Rank-local device grid.  z-slab layouts keep z ghosts of depth h and
+    x/y ghosts of depth 1; multi-axis layouts keep depth h everywhere, like
+    the reference (R/decomp.py:94-96,120-122), for the extended slabs."""
     origin = tuple(r[0] for r in decomp.ranges(rank))
     dims = decomp.local_dims(rank)
     if isinstance(pattern, FillPattern):
         pat = pattern.shifted(origin)
     else:
         pat = _ShiftedPattern(pattern, origin)
-    return TwoGrid(dims, pat, dtype=dtype, device=device, ghost_xy=1, ghost_z=decomp.halo)
+    gxy = 1 if tuple(decomp.layout[:2]) == (1, 1) else decomp.halo
+    return TwoGrid(dims, pat, dtype=dtype, device=device, ghost_xy=gxy, ghost_z=decomp.halo)
 
 
 class _ShiftedPattern:
@@ -171,23 +166,76 @@ def plane_spans(buf, lay, h: int):
     return planes(0), planes(nz - h), planes(-h), planes(nz)
 
 
-def exchange_halos_local(grids, decomp: Decomposition, h: int) -> None:
-    """All ranks' z-halo exchange in one process (R/decomp.py:149-179, z phase).
+# Phases in canonical exchange order with their array axes (R/decomp.py:125-146).
+_PHASES = (("x", 2), ("y", 1), ("z", 0))
 
-    Copies are issued after a device-wide sync of every rank's producer so a
-    cross-device copy never races the kernel that wrote its source.
+
+def build_halo_plan(halo: int):
+    """Fixed slab geometry: each phase's slab includes the ghost extensions of
+    the canonically earlier directions (R/decomp.py:137-146).  Returns
+    {name: (axis, ext)} with ext[d] = (lo, hi) extension of tangential axis d."""
+    plan = {}
+    done = set()
+    for name, axis in _PHASES:
+        plan[name] = (axis, tuple((halo, halo) if d in done else (0, 0) for d in range(3)))
+        done.add(axis)
+    return plan
+
+
+def _slab(grid: TwoGrid, axis: int, ext, rng) -> "torch.Tensor":
+    """View of ``grid.current`` over logical range ``rng`` on ``axis`` and the
+    interior (+ ext) on the tangential axes."""
+    g = (grid.gz, grid.gxy, grid.gxy)
+    n = grid.dims.shape
+    sl = []
+    for d in range(3):
+        if d == axis:
+            lo, hi = rng
+        else:
+            lo, hi = -ext[d][0], n[d] + ext[d][1]
+        sl.append(slice(lo + g[d], hi + g[d]))
+    return grid.current[tuple(sl)]
+
+
+def exchange_halos_local(grids, decomp: Decomposition, h: int, order=("x", "y", "z")) -> None:
+    """All ranks' halo exchange in one process (R/decomp.py:149-179).
+
+    Phases run in ``order`` with the canonical slab geometry, so -- as in the
+    reference -- only x -> y -> z delivers edge and corner values transitively
+    (reference test_decomp.py:195-204).  z-slab layouts move h contiguous
+    padded planes; other phases are strided device copies.  A device-wide
+    sync brackets the copies so a cross-device copy never races the kernel
+    that wrote its source.
     """
     import torch
     for g in grids:
         torch.cuda.synchronize(g.device)
-    views = [halo_planes(g, h) for g in grids]
-    for r, g in enumerate(grids):
-        lo_nb = decomp.neighbor(r, 0, high=False)
-        hi_nb = decomp.neighbor(r, 0, high=True)
-        if lo_nb is not None:
-            views[r][2].copy_(views[lo_nb][1], non_blocking=True)
-        if hi_nb is not None:
-            views[r][3].copy_(views[hi_nb][0], non_blocking=True)
+    if tuple(decomp.layout[:2]) == (1, 1):
+        views = [halo_planes(g, h) for g in grids]
+        for r in range(len(grids)):
+            lo_nb = decomp.neighbor(r, 0, high=False)
+            hi_nb = decomp.neighbor(r, 0, high=True)
+            if lo_nb is not None:
+                views[r][2].copy_(views[lo_nb][1], non_blocking=True)
+            if hi_nb is not None:
+                views[r][3].copy_(views[hi_nb][0], non_blocking=True)
+    else:
+        plan = build_halo_plan(h)
+        for name in order:
+            axis, ext = plan[name]
+            for r, g in enumerate(grids):
+                n = g.dims.shape[axis]
+                lo_nb = decomp.neighbor(r, axis, high=False)
+                hi_nb = decomp.neighbor(r, axis, high=True)
+                if lo_nb is not None:   # my low ghost <- low neighbour's top h layers
+                    nn = grids[lo_nb].dims.shape[axis]
+                    _slab(g, axis, ext, (-h, 0)).copy_(
+                        _slab(grids[lo_nb], axis, ext, (nn - h, nn)), non_blocking=True)
+                if hi_nb is not None:   # my high ghost <- high neighbour's bottom h layers
+                    _slab(g, axis, ext, (n, n + h)).copy_(
+                        _slab(grids[hi_nb], axis, ext, (0, h)), non_blocking=True)
+            for g in grids:
+                torch.cuda.synchronize(g.device)
     for g in grids:
         torch.cuda.synchronize(g.device)
 
@@ -224,11 +272,12 @@ def outer_step(grid: TwoGrid, decomp: Decomposition, rank: int,
 def run_distributed(global_dims: GridDims, pattern, layout, cfg: PipelineConfig | None,
                     outer_steps: int, h: int | None = None, order=("x", "y", "z"),
                     dtype=np.float64, devices=None):
-    """All ranks of a z-slab run in this process; returns (gathered, rank_fields).
+    """All ranks in this process; returns (gathered, rank_fields) (R/decomp.py:240-268).
 
-    The gathered interior equals outer_steps*h sweeps of the undecomposed
-    problem, bit for bit.  ``order`` is accepted for API parity: with
-    (1, 1, P) only the z phase carries data, so every order is equivalent.
+    Any layout (px, py, pz): ranks' K2 passes extend into every face with a
+    neighbour, halos move in ``order`` with the reference's extended-slab
+    geometry.  With the canonical order the gathered interior equals
+    outer_steps*h sweeps of the undecomposed problem, bit for bit.
     """
     import torch
     if h is None:
@@ -237,7 +286,6 @@ def run_distributed(global_dims: GridDims, pattern, layout, cfg: PipelineConfig 
         h = cfg.levels_per_sweep
     px, py, pz = layout
     decomp = decompose(global_dims, px * py * pz, layout, h)
-    _require_zslab(decomp.layout)
     if cfg is not None and cfg.storage != "twogrid":
         raise DecompositionError("distributed runs use two-grid storage")
     if devices is None:
@@ -245,7 +293,7 @@ def run_distributed(global_dims: GridDims, pattern, layout, cfg: PipelineConfig 
     grids = [local_grid(decomp, r, pattern, dtype=dtype, device=devices[r % len(devices)])
              for r in range(decomp.n_ranks)]
     for _ in range(outer_steps):
-        exchange_halos_local(grids, decomp, h)
+        exchange_halos_local(grids, decomp, h, order)
         for r, g in enumerate(grids):
             outer_step(g, decomp, r, cfg, h=h)
     rank_fields = [g.interior() for g in grids]

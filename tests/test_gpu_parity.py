@@ -239,9 +239,52 @@ def test_distributed_pipelined_depth_split(sp, ref_fields):
     assert bitwise(gathered, ref_fields["dist_P4_h8_s1"])
 
 
-def test_distributed_rejects_multi_axis(sp):
-    with pytest.raises(sp.DecompositionError):
-        sp.run_distributed(sp.GridDims(16, 16, 16), sp.FillPattern.random(1), (2, 1, 1), None, 1, h=1)
+# Multi-axis layouts with the x -> y -> z extended-slab exchange;
+# the cases restate the reference's own tests (test_decomp.py:169-204).
+
+def _oracle_interior(O, shape, kind, seed, levels):
+    g = O.CGrid(shape, O.BoxPattern(kind, seed=seed))
+    g.sweeps(levels)
+    return g.interior()
+
+
+def test_multi_axis_serial_matches_oracle(sp, O):
+    gathered, _ = sp.run_distributed(sp.GridDims(16, 16, 16), sp.FillPattern.random(37), (2, 2, 1),
+                                     cfg=None, outer_steps=3, h=2)
+    assert bitwise(gathered, _oracle_interior(O, (16, 16, 16), "random", 37, 6))
+
+
+def test_multi_axis_pipelined_matches_oracle(sp, O):
+    cfg = sp.PipelineConfig(teams=1, team_size=2, updates_per_thread=2, block=(24, 8, 8))
+    gathered, _ = sp.run_distributed(sp.GridDims(24, 24, 24), sp.FillPattern.random(43), (2, 1, 2),
+                                     cfg, outer_steps=2)
+    assert bitwise(gathered, _oracle_interior(O, (24, 24, 24), "random", 43, 8))
+
+
+def test_multi_axis_hotplate_walls(sp, O):
+    gathered, _ = sp.run_distributed(sp.GridDims(16, 16, 16), sp.FillPattern.hotplate(), (2, 1, 1),
+                                     cfg=None, outer_steps=2, h=4)
+    assert bitwise(gathered, _oracle_interior(O, (16, 16, 16), "hotplate", 0, 8))
+
+
+def test_multi_axis_all_three_axes(sp, O):
+    shape = (16, 18, 20)
+    faces = (1.0, 0.0, 0.5, 0.0, 0.25, 0.0)
+    pat = sp.FillPattern.dirichlet_box("random", shape, faces, seed=0)
+    gathered, _ = sp.run_distributed(sp.GridDims(20, 18, 16), pat, (2, 3, 2), cfg=None,
+                                     outer_steps=2, h=3)
+    ref = O.CGrid(shape, O.BoxPattern("random", seed=0, faces=faces, global_shape=shape))
+    ref.sweeps(6)
+    assert bitwise(gathered, ref.interior())
+
+
+def test_shuffled_phase_order_breaks_corners(sp, O):
+    gd, pat = sp.GridDims(16, 16, 16), sp.FillPattern.random(47)
+    good, _ = sp.run_distributed(gd, pat, (2, 2, 1), cfg=None, outer_steps=2, h=2, order=("x", "y", "z"))
+    bad, _ = sp.run_distributed(gd, pat, (2, 2, 1), cfg=None, outer_steps=2, h=2, order=("y", "x", "z"))
+    ref = _oracle_interior(O, (16, 16, 16), "random", 47, 4)
+    assert bitwise(good, ref)
+    assert not sp.compare(ref, bad).passed
 
 
 # ---- C1: the BASELINE parity config ----------------------------------------------------
