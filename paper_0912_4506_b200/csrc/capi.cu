@@ -213,10 +213,14 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
         auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore>;
         const size_t smem = Pl::SMEM;
-        static bool attr_set = false;  // per instantiation
-        if (!attr_set) {
+        // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
+        static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
+        int dev = 0;
+        SP_CUDA(cudaGetDevice(&dev));
+        const uint64_t bit = 1ull << (dev & 63);
+        if (!(attr_set.load() & bit)) {
             SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set = true;
+            attr_set.fetch_or(bit);
         }
         auto enc = encode_fn();
         if (!enc) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
