@@ -14,7 +14,8 @@ from .pipeline import (DEFAULT_DEPTH, PipelineConfig, PipelineTimeout, ScheduleE
                        default_block_size, run_node_sweeps, sweeps)
 from .decomp import (Decomposition, DecompositionError, decompose, level_domains_for_rank,
                      local_grid, outer_step, run_distributed)
-from .verify import Comparison, REL_TOL, F32_REL_TOL, check_maximum_principle, compare
+from .verify import (Comparison, F32_REL_TOL, REL_TOL, check_maximum_principle, compare, oracle,
+                     oracle_trajectory)
 from ._native import NativeUnavailable, build, launch_count
 
 __version__ = "0.1.0"

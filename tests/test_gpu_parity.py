@@ -357,3 +357,16 @@ def test_dump_load_round_trip(sp, O):
     sp.sweeps(h, 2, depth=1)
     ref = oracle_run(O, shape, "random", 21, None, 5)
     assert bitwise(g.interior(), ref.interior()) and bitwise(h.interior(), ref.interior())
+
+
+def test_device_oracle_api(sp, ref_fields):
+    """verify.oracle / oracle_trajectory keep the reference's names and results."""
+    traj = sp.oracle_trajectory(sp.GridDims(16, 16, 16), sp.FillPattern.random(11), 8)
+    for lv, st in enumerate(traj):
+        assert bitwise(st, ref_fields["r11_16_traj"][lv]), lv
+    g = sp.oracle(sp.GridDims(4, 4, 4), sp.FillPattern.hotplate(), 1)
+    assert bitwise(g.interior(), ref_fields["hotplate4_l1"])
+    # the temporally blocked engine agrees with the one-level engine
+    blocked = sp.TwoGrid(sp.GridDims(16, 16, 16), sp.FillPattern.random(11))
+    sp.sweeps(blocked, 8, depth=4)
+    assert sp.compare(sp.oracle(sp.GridDims(16, 16, 16), sp.FillPattern.random(11), 8), blocked).bitwise
