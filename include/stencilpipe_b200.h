@@ -128,11 +128,21 @@ int sp_digest(const void* base, int dtype, const sp_layout* L, int64_t index_bas
 int sp_probe_fp64(double* dadd_per_s, double* ms);
 
 /* Tuning hook (benchmarks only): kernel-variant override (0 = automatic per
- * dtype/T; k = variant k-1 of {16x2/2, 16x2/3, 8x4/2, 8x4/3, 8x8/2, 16x4/2}
- * = warps x rows-per-thread / z-queue slots; a variant not built for a depth
- * falls back to the first) and z-chunk count override (0 = automatic).
- * Returns the previous values encoded as variant*1000 + chunks. */
+ * dtype/T; k = variant k-1 of the table in csrc/capi.cu, warps x
+ * rows-per-thread / z-queue slots; a variant not built for a depth falls back
+ * to variant 0; -1 = single-level sweeps on the K1 kernel) and z-chunk count
+ * override (0 = automatic).  Returns the previous values encoded as
+ * (variant+1)*1000 + chunks. */
 int sp_set_tuning(int variant, int chunks);
+
+/* Tuning hook (benchmarks only): work-unit schedule of the temporally blocked
+ * kernel.  dynamic = 1: persistent CTAs claim (tile, z-chunk) units in order
+ * from a device counter, so units in flight at one time are neighbours and
+ * share their halo rows through L2; 0: static round-robin.  strip = width in
+ * tiles of the column strips units are ordered by (y-major inside a strip;
+ * 0 = plain x-major rows).  Negative arguments keep the current value.
+ * Returns the previous values encoded as dynamic*1000 + strip. */
+int sp_set_schedule(int dynamic, int strip);
 
 #ifdef __cplusplus
 }

@@ -35,7 +35,7 @@ NVCC_FLAGS = [
 # Symbols include/stencilpipe_b200.h declares (checked by the CPU tests).
 EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "sp_fill",
            "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_run_sweeps",
-           "sp_digest", "sp_probe_fp64", "sp_set_tuning")
+           "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule")
 
 
 class NativeUnavailable(RuntimeError):
@@ -94,6 +94,7 @@ def load_library():
     if not os.path.exists(LIB_PATH):
         raise NativeUnavailable(f"{LIB_PATH} is not built; run __graft_entry__.build()")
     L = ctypes.CDLL(LIB_PATH)
+    override = bool(os.environ.get("SP_LIB_PATH"))
     P = ctypes.POINTER
     vp = ctypes.c_void_p
     i64p = P(ctypes.c_int64)
@@ -114,7 +115,11 @@ def load_library():
     L.sp_probe_fp64.argtypes = [P(ctypes.c_double), P(ctypes.c_double)]
     L.sp_set_tuning.argtypes = [ctypes.c_int, ctypes.c_int]
     for name in EXPORTS:
+        if override and not hasattr(L, name):
+            continue   # older library under A/B comparison: tuning hooks may be absent
         getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
+    if hasattr(L, "sp_set_schedule") or not override:
+        L.sp_set_schedule.argtypes = [ctypes.c_int, ctypes.c_int]
     _lib = L
     return L
 

@@ -24,6 +24,8 @@ thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
 int g_chunks = 0;
 int g_use_k1 = 0;   // 1: single-level sweeps use the L1-streaming K1 kernel instead of K2(T=1)
+int g_dynamic = 1;  // K2 unit schedule: 1 = claimed in order from a device counter, 0 = round-robin
+int g_strip = 0;    // K2 unit order: tile-column strips this wide (0 = x-major rows)
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -93,6 +95,30 @@ int check_layout(const sp_layout* L, int dtype) {
     return SP_OK;
 }
 
+// Dynamic-schedule unit counters: kCounters per device, zeroed once; each
+// K2 launch takes the next one (launches on different streams may overlap)
+// and the kernel leaves it at zero again.  Reuse needs kCounters launches in
+// flight at once.
+constexpr int kCounters = 1024;
+
+int sched_counter(unsigned** out) {
+    static std::mutex mu;
+    static unsigned* base[64] = {};
+    static uint32_t next[64] = {};
+    int dev = 0;
+    SP_CUDA(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= 64) return fail(SP_ERR_DEVICE, "device ordinal %d out of range", dev);
+    std::lock_guard<std::mutex> lock(mu);
+    if (!base[dev]) {
+        unsigned* p = nullptr;
+        SP_CUDA(cudaMalloc(&p, kCounters * sizeof(unsigned)));
+        SP_CUDA(cudaMemset(p, 0, kCounters * sizeof(unsigned)));
+        base[dev] = p;
+    }
+    *out = base[dev] + (next[dev]++ % kCounters);
+    return SP_OK;
+}
+
 // Kernel variants: CTA shape (warps BY x rows-per-thread PY; footprint is
 // 64 x BY*PY) and z-queue depth (2 = shift by moves, 3 = rotating registers).
 struct Variant {
@@ -101,7 +127,7 @@ struct Variant {
 };
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0},  // 0: fallback for every depth
-    {16, 2, 3, 1, 8, 0},  // 1: fp64 T=2 default
+    {16, 2, 3, 1, 8, 0},  // 1
     {8, 4, 2, 1, 8, 0},   // 2: fp64 T=4 default, fp32 T>4
     {8, 4, 3, 1, 8, 0},   // 3: fp64 T=3 default
     {8, 8, 2, 1, 8, 0},   // 4: fp32 T=3 default (64x64 footprint)
@@ -109,8 +135,10 @@ constexpr Variant kVariants[] = {
     {16, 2, 1, 1, 8, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
     {8, 4, 1, 1, 8, 0},   // 7: same, 8 warps
     {8, 8, 2, 1, 8, 1},   // 8: fp32 T=4 default: 4 with the running output pointer
+    {8, 4, 2, 2, 8, 0},   // 9: fp64 T=2 default: two CTAs per SM (<= 128 registers)
+    {8, 4, 1, 2, 8, 0},   // 10: two CTAs per SM, z-queue v[p-1] from shared memory
 };
-constexpr int kNumVariants = 9;
+constexpr int kNumVariants = 11;
 int g_variant_override = -1;
 
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
@@ -119,6 +147,7 @@ template <typename R, int T, int V>
 constexpr bool compiled() {
     if (V == 0) return true;
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
+    if (V >= 9) return T >= 2 && T <= 4;
     if (T == 1) return V == 5 || V == 1;
     if (sizeof(R) == 8) {
         if (T == 2) return V == 1 || V == 3 || V == 4 || V >= 6;
@@ -131,12 +160,12 @@ constexpr bool compiled() {
 }
 
 // Default variant per (dtype, T), from the B200 tuning runs (DESIGN.md,
-// profiles/tuning_r01.md): fp64 T=2 16x2/3, T=3 8x4/3, T=4 8x4/2; fp32 T<=2
-// 16x2, T=3..4 8x8/2, deeper 8x4/2.
+// profiles/r01_tuning.md): fp64 T=2 8x4/2 at two CTAs per SM, T=3 8x4/3,
+// T=4 8x4/2; fp32 T<=2 16x2, T=3..4 8x8/2, deeper 8x4/2.
 int default_variant(int dtype, int T) {
     if (T == 1) return dtype == SP_F64 ? 5 : 1;
     if (dtype == SP_F64) {
-        if (T == 2) return 1;
+        if (T == 2) return 9;
         if (T == 3) return 3;
         if (T == 4) return 2;
         return 0;
@@ -145,20 +174,6 @@ int default_variant(int dtype, int T) {
     if (T == 3) return 4;
     if (T == 4) return 8;
     return 2;
-}
-
-// Host mirror of sp::Plan<>::FITS.
-bool variant_fits(int dtype, int T, int v) {
-    const int es = elem_size(dtype);
-    const int wy = kVariants[v].by * kVariants[v].py;
-    const int minb = kVariants[v].minb;
-    const int plane = sp::WX * wy * es, nl = T > 1 ? T - 1 : 0;
-    const int budget = (minb == 1 ? 232448 : 233472 / minb - 1024) - 256;
-    const int nbuf = (2 * nl + 3) * plane <= budget ? 2 : 1;
-    int ring = budget / plane - nbuf * nl;
-    if (ring > kVariants[v].ring) ring = kVariants[v].ring;
-    const bool smemq = kVariants[v].slots == 1;
-    return ring >= (smemq ? 4 : 3) && wy - 2 * T >= 1 && (!smemq || nbuf == 2);
 }
 
 template <typename R, int T, int V>
@@ -178,7 +193,9 @@ bool is_usable(int v) {
         case 5: return usable<R, T, 5>();
         case 6: return usable<R, T, 6>();
         case 7: return usable<R, T, 7>();
-        default: return usable<R, T, 8>();
+        case 8: return usable<R, T, 8>();
+        case 9: return usable<R, T, 9>();
+        default: return usable<R, T, 10>();
     }
 }
 
@@ -255,7 +272,9 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 5: return launch_tb_t<R, T, 5>(src, L, a, grid, s);
         case 6: return launch_tb_t<R, T, 6>(src, L, a, grid, s);
         case 7: return launch_tb_t<R, T, 7>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 8>(src, L, a, grid, s);
+        case 8: return launch_tb_t<R, T, 8>(src, L, a, grid, s);
+        case 9: return launch_tb_t<R, T, 9>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 10>(src, L, a, grid, s);
     }
 }
 
@@ -291,6 +310,13 @@ int sp_set_tuning(int variant, int chunks) {
     g_chunks = chunks;
     g_use_k1 = variant < 0 ? 1 : 0;   // variant -1: K1 for single-level sweeps
     if (variant < 0) g_variant_override = -1;
+    return prev;
+}
+
+int sp_set_schedule(int dynamic, int strip) {
+    int prev = g_dynamic * 1000 + g_strip;
+    if (dynamic >= 0) g_dynamic = dynamic ? 1 : 0;
+    if (strip >= 0) g_strip = strip;
     return prev;
 }
 
@@ -413,9 +439,15 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
     if (g_chunks > 0) best_n = std::min<int64_t>(g_chunks, nzb);
     int64_t len = (nzb + best_n - 1) / best_n;
     int64_t nch = (nzb + len - 1) / len;
-    if (tiles * nch >= (1ll << 31)) return fail(SP_ERR_SCHEDULE, "too many work units");
+    if (tiles * nch >= (1ll << 31) - (1 << 20)) return fail(SP_ERR_SCHEDULE, "too many work units");
     a.chunk_len = (int)len;
     a.units = (int)(tiles * nch);
+    a.strip = g_strip;
+    a.sched = nullptr;
+    if (g_dynamic) {
+        rc = sched_counter(&a.sched);
+        if (rc) return rc;
+    }
     int grid = (int)std::min<int64_t>(a.units, slots);
     cudaStream_t s = (cudaStream_t)stream;
     if (dtype == SP_F64) return launch_tb<double>(T, variant, src, L, a, grid, s);

@@ -46,6 +46,8 @@ struct TBArgs {
     int ox, oy;                // output tile extents (<= WX-2T-(A-1), WY-2T)
     int x_off, gy, gz;         // TMA coordinate offsets of interior (0,0,0)
     int align;                 // elements per 16 bytes (TMA box start alignment)
+    unsigned* sched;           // unit counter (dynamic schedule; zero on entry and exit) or null
+    int strip;                 // unit order: tile-column strips of this width, y-major (0: x-major)
 };
 
 // ---- small PTX helpers ------------------------------------------------------
@@ -79,6 +81,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!ok);
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2) {
     asm volatile(
@@ -109,12 +115,25 @@ struct Unit {
     int x0, y0, zc0, zc1;
 };
 
+// Units are z-chunk major; inside a chunk, tiles go y-major through column
+// strips `strip` tiles wide, so consecutive units are x/y neighbours (their
+// footprints share halo rows) -- under the dynamic schedule they are in
+// flight together and the shared rows come from L2.
 __device__ __forceinline__ Unit decode_unit(const TBArgs& a, int u) {
     int per = a.ntx * a.nty;
     int c = u / per;
     int r = u - c * per;
-    int ty = r / a.ntx;
-    int tx = r - ty * a.ntx;
+    int tx, ty;
+    if (a.strip > 0) {
+        const int s = r / (a.strip * a.nty);
+        const int k = r - s * (a.strip * a.nty);
+        const int sw = min(a.strip, a.ntx - s * a.strip);
+        ty = k / sw;
+        tx = s * a.strip + (k - ty * sw);
+    } else {
+        ty = r / a.ntx;
+        tx = r - ty * a.ntx;
+    }
     Unit w;
     w.x0 = a.olo[2] + tx * a.ox;
     w.y0 = a.olo[1] + ty * a.oy;
@@ -154,7 +173,8 @@ struct Plan {
     static constexpr int RING = RING_FIT > RCAP ? RCAP : RING_FIT;
     static constexpr int MIN_RING = SLOTS == 1 ? 4 : 3;
     static constexpr bool FITS = RING >= MIN_RING && WY - 2 * T >= 1 && (SLOTS != 1 || DB);
-    static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + RING * 8;
+    static constexpr int NUID = 16;   // unit ids handed from the producer to the consumers
+    static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + RING * 8 + NUID * 4;
 };
 
 template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE>
@@ -173,6 +193,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     R* ring = reinterpret_cast<R*>(smem_raw);
     R* lvl = ring + RING_N * PLANE;  // [level-1][buf] planes for levels 1..T-1
     uint64_t* full = reinterpret_cast<uint64_t*>(lvl + P::NBUF * P::NL * PLANE);
+    volatile int* uid = reinterpret_cast<volatile int*>(full + RING_N);
 
     const int lane = threadIdx.x & 31;
     const int wy = threadIdx.x >> 5;
@@ -188,10 +209,24 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     }
     __syncthreads();
 
-    // Producer cursor (thread 0 only): walks the same (unit, step) sequence.
-    // TMA coordinates (c0, c1, c2) of the next plane and the unit's last c2.
-    int pu = blockIdx.x, pc0 = 0, pc1 = 0, pc2 = 0, pc2_end = 0;
+    // Producer (thread 0 only): claims units -- from the device counter
+    // (dynamic) or round-robin (static) -- publishes each id in uid[] ahead
+    // of the unit's first TMA (the mbarrier arrive releases it to the
+    // consumers) and walks the unit's planes: TMA coordinates (c0, c1, c2)
+    // of the next plane and the unit's last c2.  After the last unit, one
+    // plain arrive completes the next slot's phase so the consumers can read
+    // the end marker (-1).
+    int pu = -1, pseq = 0, pc0 = 0, pc1 = 0, pc2 = 0, pc2_end = 0;
+    bool pdone = false;
     auto producer_unit = [&]() {
+        if (a.sched) {
+            pu = (int)atomicAdd(a.sched, 1u);
+            // every CTA overshoots exactly once; the last overshoot re-arms the counter
+            if (pu == a.units + (int)gridDim.x - 1) atomicExch(a.sched, 0u);
+        } else {
+            pu = pseq == 0 ? (int)blockIdx.x : pu + (int)gridDim.x;
+        }
+        uid[pseq++ & (P::NUID - 1)] = pu < a.units ? pu : -1;
         if (pu >= a.units) return;
         const Unit pw = decode_unit(a, pu);
         pc0 = footprint_x<R>(a, pw.x0, T) + a.x_off;
@@ -199,15 +234,16 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         pc2 = pw.zc0 - T + a.gz;
         pc2_end = pw.zc1 + T + a.gz;
     };
-    producer_unit();
+    if (threadIdx.x == 0) producer_unit();
     auto produce = [&](int slot) {
-        if (pu >= a.units) return;
+        if (pu >= a.units) {
+            if (!pdone) mbar_arrive(&full[slot]);
+            pdone = true;
+            return;
+        }
         mbar_expect_tx(&full[slot], kPlaneBytes);
         tma_load_3d(ring + slot * PLANE, &tmap, &full[slot], pc0, pc1, pc2);
-        if (++pc2 == pc2_end) {
-            pu += gridDim.x;
-            producer_unit();
-        }
+        if (++pc2 == pc2_end) producer_unit();
     };
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
@@ -218,7 +254,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     const R sixth = A::sixth();
     uint32_t gstep = 0;
 
-    for (int u = blockIdx.x; u < a.units; u += gridDim.x) {
+    for (int cseq = 0;; ++cseq) {
+        // the unit's first plane (or the end marker) has landed: its id is published
+        mbar_wait(&full[gstep % RING_N], (gstep / RING_N) & 1);
+        const int u = uid[cseq & (P::NUID - 1)];
+        if (u < 0) break;
         const Unit w = decode_unit(a, u);
         const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T;
         const int nsteps = (w.zc1 - w.zc0) + 2 * T;

@@ -17,12 +17,15 @@ ap.add_argument("--depth", type=int, default=2)
 ap.add_argument("--shape", type=int, default=0)
 ap.add_argument("--passes", type=int, default=3)
 ap.add_argument("--chunks", type=int, default=0)
+ap.add_argument("--sched", default="", help="dynamic:strip")
 args = ap.parse_args()
 dt = np.float64 if args.dtype == "f64" else np.float32
 n, nz = args.n, args.nz or args.n
 pat = sp.FillPattern.dirichlet_box("random", (nz, n, n), (1.0, 0, 0.5, 0, 0.25, 0))
 g = sp.TwoGrid(sp.GridDims(n, n, nz), pat, dtype=dt)
 sp._native.lib().sp_set_tuning(args.shape, args.chunks)
+if args.sched:
+    sp._native.lib().sp_set_schedule(*(int(v) for v in args.sched.split(":")))
 for _ in range(args.passes):
     sp.sweeps(g, args.depth, depth=args.depth)
 torch.cuda.synchronize()

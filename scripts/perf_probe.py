@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--depths", default="1,2,3,4,5,6,8")
     ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--shapes", default="0", help="comma list: 0=auto, k=shape k-1")
+    ap.add_argument("--sched", default="", help="comma list of dynamic:strip (sp_set_schedule)")
     args = ap.parse_args()
     dt = np.float64 if args.dtype == "f64" else np.float32
     n = args.n
@@ -38,8 +39,13 @@ def main():
     ms = ctypes.c_double()
     sp._native.check(sp._native.lib().sp_probe_fp64(ctypes.byref(rate), ctypes.byref(ms)))
     out["fp64_dadd_per_s"] = rate.value
-    for shape in [int(v) for v in args.shapes.split(",")]:
+    combos = [(sh, sc) for sc in (args.sched.split(",") if args.sched else [""])
+              for sh in [int(v) for v in args.shapes.split(",")]]
+    for shape, sc in combos:
       sp._native.lib().sp_set_tuning(shape, args.chunks)
+      if sc:
+        dyn, strip = (int(v) for v in sc.split(":"))
+        sp._native.lib().sp_set_schedule(dyn, strip)
       for depth in [int(d) for d in args.depths.split(",")]:
         levels = (args.levels // depth) * depth
         sp.sweeps(g, depth, depth=depth)   # warm-up (JIT attr, TMA descriptors)
@@ -53,9 +59,10 @@ def main():
         t = e0.elapsed_time(e1) / 1e3
         glups = n * n * nz * levels / t / 1e9
         es = 8 if dt == np.float64 else 4
-        out[f"S{shape}T{depth}"] = {"glups": round(glups, 1), "ms_per_pass": round(t / (levels // depth) * 1e3, 3),
+        key = f"S{shape}T{depth}" + (f"@{sc}" if sc else "")
+        out[key] = {"glups": round(glups, 1), "ms_per_pass": round(t / (levels // depth) * 1e3, 3),
                             "hbm_equiv_gbs": round(glups * 2 * es / depth, 1)}
-        print(shape, depth, out[f"S{shape}T{depth}"], flush=True)
+        print(shape, depth, sc, out[key], flush=True)
     print(json.dumps(out))
 
 

@@ -299,7 +299,7 @@ def test_c1_full_grid_vs_reference(sp, kat, ref_fields):
     assert bitwise(inner[kat["c1_planes_index"]], ref_fields["c1_planes_l100"])
 
 
-@pytest.mark.parametrize("shape_id", list(range(1, 10)))
+@pytest.mark.parametrize("shape_id", list(range(1, 12)))
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_every_cta_shape(sp, O, shape_id, dtype):
     lib = sp._native.lib()
@@ -370,3 +370,33 @@ def test_device_oracle_api(sp, ref_fields):
     blocked = sp.TwoGrid(sp.GridDims(16, 16, 16), sp.FillPattern.random(11))
     sp.sweeps(blocked, 8, depth=4)
     assert sp.compare(sp.oracle(sp.GridDims(16, 16, 16), sp.FillPattern.random(11), 8), blocked).bitwise
+
+
+@pytest.mark.parametrize("sched", [(0, 0), (1, 0), (1, 3), (0, 5)])
+def test_unit_schedules(sp, O, sched):
+    """Static/dynamic unit claiming and strip orders give identical fields."""
+    lib = sp._native.lib()
+    prev = lib.sp_set_schedule(*sched)
+    try:
+        for shape, levels, depth, chunks in [((40, 70, 130), 8, 4, 0), ((70, 65, 190), 10, 2, 7),
+                                             ((33, 31, 29), 6, 3, 29), ((5, 200, 300), 4, 2, 1)]:
+            lib.sp_set_tuning(0, chunks)
+            faces = (0.3, -1.0, 2.0, 0.0, 1.0, -0.5)
+            g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, faces, seed=5))
+            sp.sweeps(g, levels, depth=depth)
+            ref = oracle_run(O, shape, "random", 5, faces, levels)
+            assert bitwise(g.interior(), ref.interior()), (sched, shape, chunks)
+    finally:
+        lib.sp_set_tuning(0, 0)
+        lib.sp_set_schedule(prev // 1000, prev % 1000)
+
+
+def test_dynamic_counter_rearms(sp, O):
+    """More launches than unit counters: every counter must be back at zero for reuse."""
+    shape = (6, 20, 70)
+    faces = (1.0, 0.0, 0.5, 0.0, 0.25, 0.0)
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, faces, seed=9))
+    levels = 2 * 1100
+    sp.sweeps(g, levels, depth=2)
+    ref = oracle_run(O, shape, "random", 9, faces, levels)
+    assert bitwise(g.interior(), ref.interior())
