@@ -120,25 +120,34 @@ int sched_counter(unsigned** out) {
 }
 
 // Kernel variants: CTA shape (warps BY x rows-per-thread PY; footprint is
-// 64 x BY*PY) and z-queue depth (2 = shift by moves, 3 = rotating registers).
+// 64 x BY*PY), z-queue depth (2 = shift by moves, 3 = rotating registers,
+// 1 = v[p-1] re-read from shared memory), CTAs per SM, TMA ring cap, running
+// output pointer, and the step synchronisation (split = per-warp mbarrier
+// arrive/wait on the level planes instead of one __syncthreads per step).
 struct Variant {
     int by, py, slots, minb, ring;   // warps, rows/thread, z-queue slots, CTAs/SM, TMA ring cap
     int rstore;                      // 1: running output pointer (see tb_kernel)
+    int split;                       // 1: split step barrier (see tb_kernel)
 };
 constexpr Variant kVariants[] = {
-    {16, 2, 2, 1, 8, 0},  // 0: fallback for every depth
-    {16, 2, 3, 1, 8, 0},  // 1
-    {8, 4, 2, 1, 8, 0},   // 2: fp64 T=4 default, fp32 T>4
-    {8, 4, 3, 1, 8, 0},   // 3: fp64 T=3 default
-    {8, 8, 2, 1, 8, 0},   // 4: fp32 T=3 default (64x64 footprint)
-    {16, 2, 3, 1, 6, 0},  // 5: T=1 default (shallower ring streams better)
-    {16, 2, 1, 1, 8, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
-    {8, 4, 1, 1, 8, 0},   // 7: same, 8 warps
-    {8, 8, 2, 1, 8, 1},   // 8: fp32 T=4 default: 4 with the running output pointer
-    {8, 4, 2, 2, 8, 0},   // 9: fp64 T=2 default: two CTAs per SM (<= 128 registers)
-    {8, 4, 1, 2, 8, 0},   // 10: two CTAs per SM, z-queue v[p-1] from shared memory
+    {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
+    {16, 2, 3, 1, 8, 0, 1},  // 1: fp64 T=3
+    {8, 4, 2, 1, 8, 0, 0},   // 2: fp32 T>6
+    {8, 4, 3, 1, 8, 0, 1},   // 3: fp64 T=4
+    {8, 8, 2, 1, 8, 0, 0},   // 4: fp32 T=2 (64x64 footprint)
+    {16, 2, 3, 1, 6, 0, 0},  // 5: fp64 T=1 (shallower ring streams better)
+    {16, 2, 1, 1, 8, 0, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
+    {8, 4, 1, 1, 8, 0, 0},   // 7: same, 8 warps
+    {8, 8, 2, 1, 8, 1, 0},   // 8: fp32 T=3,4: 4 with the running output pointer
+    {8, 4, 2, 2, 8, 0, 1},   // 9: fp64 T=2: two CTAs per SM (<= 128 registers), split
+    {8, 4, 1, 2, 8, 0, 0},   // 10: two CTAs per SM, z-queue v[p-1] from shared memory
+    {16, 2, 2, 1, 8, 0, 1},  // 11: fp32 T=5,6: 0 with the split barrier
+    {8, 4, 2, 1, 8, 0, 1},   // 12: fp64 T>4: 2 with the split barrier
+    {8, 4, 3, 1, 8, 0, 0},   // 13: 3 with __syncthreads
+    {16, 2, 3, 1, 8, 0, 0},  // 14: fp32 T=1: 1 with __syncthreads
 };
-constexpr int kNumVariants = 11;
+constexpr int kNumVariants = 15;
+static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
@@ -146,34 +155,36 @@ int g_variant_override = -1;
 template <typename R, int T, int V>
 constexpr bool compiled() {
     if (V == 0) return true;
+    if (T == 1) return V == 5 || V == 14;
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
-    if (V >= 9) return T >= 2 && T <= 4;
-    if (T == 1) return V == 5 || V == 1;
-    if (sizeof(R) == 8) {
-        if (T == 2) return V == 1 || V == 3 || V == 4 || V >= 6;
-        if (T <= 4) return V == 2 || V == 3 || V >= 6;
-        return false;
-    }
-    if (T == 2) return V == 1 || V == 3 || V == 4 || V >= 6;
-    if (T <= 4) return V == 2 || V == 3 || V == 4 || V >= 6;
-    return V == 2;
+    if (V == 9 || V == 10) return T <= 4;
+    if (V == 11) return true;
+    if (V == 4) return T <= 4;
+    if (V == 2 || V == 12) return T >= 3;
+    return T <= 4;
 }
 
-// Default variant per (dtype, T), from the B200 tuning runs (DESIGN.md,
-// profiles/r01_tuning.md): fp64 T=2 8x4/2 at two CTAs per SM, T=3 8x4/3,
-// T=4 8x4/2; fp32 T<=2 16x2, T=3..4 8x8/2, deeper 8x4/2.
+// Default variant per (dtype, T), from same-box B200 sweeps
+// (profiles/r01_tuning.md, "split barrier" table).
 int default_variant(int dtype, int T) {
-    if (T == 1) return dtype == SP_F64 ? 5 : 1;
     if (dtype == SP_F64) {
-        if (T == 2) return 9;
-        if (T == 3) return 3;
-        if (T == 4) return 2;
-        return 0;
+        switch (T) {
+            case 1: return 5;    // 16x2/3, ring 6
+            case 2: return 9;    // 8x4/2, two CTAs per SM, split
+            case 3: return 1;    // 16x2/3, split
+            case 4: return 3;    // 8x4/3, split
+            default: return 12;  // 8x4/2, split
+        }
     }
-    if (T == 2) return 0;
-    if (T == 3) return 4;
-    if (T == 4) return 8;
-    return 2;
+    switch (T) {
+        case 1: return 14;       // 16x2/3
+        case 2: return 4;        // 8x8/2 (64x64 footprint)
+        case 3:
+        case 4: return 8;        // 8x8/2, running output pointer
+        case 5:
+        case 6: return 11;       // 16x2/2, split
+        default: return 2;       // 8x4/2
+    }
 }
 
 template <typename R, int T, int V>
@@ -195,7 +206,11 @@ bool is_usable(int v) {
         case 7: return usable<R, T, 7>();
         case 8: return usable<R, T, 8>();
         case 9: return usable<R, T, 9>();
-        default: return usable<R, T, 10>();
+        case 10: return usable<R, T, 10>();
+        case 11: return usable<R, T, 11>();
+        case 12: return usable<R, T, 12>();
+        case 13: return usable<R, T, 13>();
+        default: return usable<R, T, 14>();
     }
 }
 
@@ -228,7 +243,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
     } else {
         constexpr Variant v = kVariants[V];
         using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore>;
+        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split>;
         const size_t smem = Pl::SMEM;
         // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
         static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
@@ -274,7 +289,11 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 7: return launch_tb_t<R, T, 7>(src, L, a, grid, s);
         case 8: return launch_tb_t<R, T, 8>(src, L, a, grid, s);
         case 9: return launch_tb_t<R, T, 9>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 10>(src, L, a, grid, s);
+        case 10: return launch_tb_t<R, T, 10>(src, L, a, grid, s);
+        case 11: return launch_tb_t<R, T, 11>(src, L, a, grid, s);
+        case 12: return launch_tb_t<R, T, 12>(src, L, a, grid, s);
+        case 13: return launch_tb_t<R, T, 13>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 14>(src, L, a, grid, s);
     }
 }
 

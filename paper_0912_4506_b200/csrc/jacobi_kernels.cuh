@@ -174,10 +174,10 @@ struct Plan {
     static constexpr int MIN_RING = SLOTS == 1 ? 4 : 3;
     static constexpr bool FITS = RING >= MIN_RING && WY - 2 * T >= 1 && (SLOTS != 1 || DB);
     static constexpr int NUID = 16;   // unit ids handed from the producer to the consumers
-    static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + RING * 8 + NUID * 4;
+    static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + (RING + 2) * 8 + NUID * 4;
 };
 
-template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE>
+template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
@@ -193,7 +193,15 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     R* ring = reinterpret_cast<R*>(smem_raw);
     R* lvl = ring + RING_N * PLANE;  // [level-1][buf] planes for levels 1..T-1
     uint64_t* full = reinterpret_cast<uint64_t*>(lvl + P::NBUF * P::NL * PLANE);
-    volatile int* uid = reinterpret_cast<volatile int*>(full + RING_N);
+    uint64_t* lbar = full + RING_N;   // [2]: step-parity barriers of the level planes (SPLIT)
+    volatile int* uid = reinterpret_cast<volatile int*>(lbar + 2);
+    // SPLIT: instead of one __syncthreads per z-step, each warp arrives on
+    // lbar[step & 1] when it has finished the step, and waits for the
+    // previous step's arrivals only where it first touches the level planes
+    // (the level-1 edge-row store).  The TMA wait, ring loads and level-1
+    // arithmetic of step k overlap the slowest warps of step k-1; thread 0
+    // refills the ring slot freed by step k-1 right after that wait.
+    constexpr bool SPLIT = SPLITV && T >= 2 && P::DB && SLOTS != 1;
 
     const int lane = threadIdx.x & 31;
     const int wy = threadIdx.x >> 5;
@@ -205,6 +213,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < RING_N; ++i) mbar_init(&full[i], 1);
+        mbar_init(&lbar[0], BY);
+        mbar_init(&lbar[1], BY);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -432,6 +442,16 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                             Q[1][t - 1][j][i] = nn[j][i];
                         }
                     }
+                if (SPLIT && t == 1 && gstep > 0) {
+                    // step k-1 is complete in every warp: its reads of this
+                    // buffer are done and its level planes are visible
+                    const uint32_t k1 = gstep - 1;
+                    mbar_wait(&lbar[k1 & 1u], (k1 >> 1) & 1u);
+                    if (threadIdx.x == 0) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        produce(pslot2);   // ring slot of plane k-2, last read in step k-1
+                    }
+                }
                 if (t < T) {
                     R* Pl = lvl + ((t - 1) * P::NBUF + cur) * PLANE;
                     if constexpr (SLOTS == 1) {
@@ -476,11 +496,16 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 }
             }
             if (RSTORE) dnext += pz;
-            __syncthreads();
-            // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
-            if (threadIdx.x == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                produce(SLOTS == 1 ? pslot2 : pslot);
+            if constexpr (SPLIT) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&lbar[gstep & 1u]);
+            } else {
+                __syncthreads();
+                // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
+                if (threadIdx.x == 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    produce(SLOTS == 1 ? pslot2 : pslot);
+                }
             }
             ++gstep;
         };
