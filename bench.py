@@ -205,6 +205,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--slab-runner", action="store_true",
+                    help="dev: use the multi-GPU SlabRunner path even at N=1 (run under torchrun)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -223,7 +225,8 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
-    if world > 1:
+    use_runner = world > 1 or args.slab_runner
+    if use_runner:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
 
@@ -250,7 +253,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     pass_events = []
 
-    if world == 1:
+    if not use_runner:
         grid = sp.TwoGrid(sp.GridDims(nx, ny, nz), pat, dtype=dtype, device=dev)
 
         def step(record=False):
@@ -331,11 +334,14 @@ def main():
 
     # --- e2e: the public API with host buffers ---
     e2e = None
-    if rank == 0 and world == 1 and not args.no_e2e:
-        e2e = measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=max(args.steps, 3))
+    if not args.no_e2e:
+        if not use_runner:
+            e2e = measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=max(args.steps, 3))
+        else:
+            e2e = measure_e2e_dist(torch, dist, runner, passes, dev, world, steps=max(args.steps, 3))
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not args.slab_runner:
         v, cores, sample = cpu_sample(shape, kind, faces, dt, budget_s=args.cpu_seconds)
         cpu = {"value": round(v, 3), "unit": "GLUP/s", "cores": cores, "kind": "port",
                "sample": sample}
@@ -379,6 +385,50 @@ def main():
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def measure_e2e_dist(torch, dist, runner, passes, dev, world, steps=3):
+    """e2e at N GPUs: every rank uploads its ghosted z-slab from pinned host
+    memory, runs the sweeps through SlabRunner (NCCL halos), and reads its
+    interior back; time is the max over ranks (barrier on both sides)."""
+    g = runner.grid
+    cuda = torch.device(dev).type == "cuda"       # CPU only in the gloo test of this function
+    host_in = torch.empty(tuple(g.current.shape), dtype=g.torch_dtype, pin_memory=cuda)
+    host_in.copy_(g.current.cpu())                 # this rank's current field (untimed)
+    host_out = torch.empty(tuple(g.dims.shape), dtype=g.torch_dtype, pin_memory=cuda)
+
+    def sync():
+        if cuda:
+            torch.cuda.synchronize(dev)
+
+    def one():
+        g.active = 0
+        g.current.copy_(host_in, non_blocking=True)          # H2D
+        g.other.copy_(g.current, non_blocking=True)          # B = copy of A (R/grid.py:132-133)
+        for t in passes:
+            runner.step(levels=t)
+        runner.finish()
+        host_out.copy_(g.interior_device(), non_blocking=True)   # D2H
+
+    one()
+    sync()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    sync()
+    el = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+    dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    el = float(el.item())
+    d = g.dims
+    lups = d.nx * d.ny * d.nz * sum(passes) * steps * world
+    es = host_in.element_size()
+    return {"value": round(lups / el / 1e9, 2), "unit": "GLUP/s",
+            "h2d_bytes_per_step": host_in.numel() * es * world,
+            "d2h_bytes_per_step": host_out.numel() * es * world,
+            "steps": steps, "ms_per_step": round(el / steps * 1e3, 2),
+            "api": "per rank: slab.current.copy_(pinned) -> SlabRunner.step() x passes (NCCL halos) "
+                   "-> interior_device() -> pinned; max over ranks"}
 
 
 def measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=3):

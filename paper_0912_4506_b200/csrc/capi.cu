@@ -133,7 +133,7 @@ constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
     {16, 2, 3, 1, 8, 0, 1},  // 1: fp64 T=3
     {8, 4, 2, 1, 8, 0, 0},   // 2: fp32 T>6
-    {8, 4, 3, 1, 8, 0, 1},   // 3: fp64 T=4
+    {8, 4, 3, 1, 8, 0, 1},   // 3
     {8, 8, 2, 1, 8, 0, 0},   // 4: fp32 T=2 (64x64 footprint)
     {16, 2, 3, 1, 6, 0, 0},  // 5: fp64 T=1 (shallower ring streams better)
     {16, 2, 1, 1, 8, 0, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
@@ -145,8 +145,9 @@ constexpr Variant kVariants[] = {
     {8, 4, 2, 1, 8, 0, 1},   // 12: fp64 T>4: 2 with the split barrier
     {8, 4, 3, 1, 8, 0, 0},   // 13: 3 with __syncthreads
     {16, 2, 3, 1, 8, 0, 0},  // 14: fp32 T=1: 1 with __syncthreads
+    {8, 4, 3, 1, 8, 1, 1},   // 15: fp64 T=4: 3 with the running output pointer
 };
-constexpr int kNumVariants = 15;
+constexpr int kNumVariants = 16;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
@@ -172,7 +173,7 @@ int default_variant(int dtype, int T) {
             case 1: return 5;    // 16x2/3, ring 6
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
             case 3: return 1;    // 16x2/3, split
-            case 4: return 3;    // 8x4/3, split
+            case 4: return 15;   // 8x4/3, split, running output pointer
             default: return 12;  // 8x4/2, split
         }
     }
@@ -210,7 +211,8 @@ bool is_usable(int v) {
         case 11: return usable<R, T, 11>();
         case 12: return usable<R, T, 12>();
         case 13: return usable<R, T, 13>();
-        default: return usable<R, T, 14>();
+        case 14: return usable<R, T, 14>();
+        default: return usable<R, T, 15>();
     }
 }
 
@@ -293,7 +295,8 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 11: return launch_tb_t<R, T, 11>(src, L, a, grid, s);
         case 12: return launch_tb_t<R, T, 12>(src, L, a, grid, s);
         case 13: return launch_tb_t<R, T, 13>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 14>(src, L, a, grid, s);
+        case 14: return launch_tb_t<R, T, 14>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 15>(src, L, a, grid, s);
     }
 }
 

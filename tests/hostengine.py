@@ -39,6 +39,21 @@ class HostGrid:
         self._b.copy_(self._a)
         self.active = 0
 
+    @property
+    def torch_dtype(self):
+        return self._a.dtype
+
+    @property
+    def current(self):
+        return self.current_buffer()
+
+    @property
+    def other(self):
+        return self.other_buffer()
+
+    def interior_device(self):
+        return torch.from_numpy(self.interior())
+
     def current_buffer(self):
         return self._a if self.active == 0 else self._b
 

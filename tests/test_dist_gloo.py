@@ -84,3 +84,50 @@ def test_three_ranks_with_remainder_step(O):
     g = O.CGrid((40, 10, 12), O.BoxPattern("random", seed=0, faces=Z1, global_shape=(40, 10, 12)))
     g.sweeps(11)
     assert np.array_equal(full.view(np.uint64), g.interior().view(np.uint64))
+
+
+def _e2e_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import torch
+    import torch.distributed as dist
+    import bench
+    from hostengine import HostEngine
+    from oracle import oracle as O
+    import paper_0912_4506_b200 as sp
+    from paper_0912_4506_b200.dist import SlabRunner
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        gshape = (40, 10, 12)
+        base = O.BoxPattern("random", seed=0, faces=Z1, global_shape=gshape)
+        r = SlabRunner(sp.GridDims(12, 10, 40), None, h=4, dtype=np.float64, depth=4,
+                       engine=HostEngine(base))
+        e2e = bench.measure_e2e_dist(torch, dist, r, [4, 4], torch.device("cpu"), world, steps=2)
+        full = r.gather()
+        if rank == 0:
+            q.put((full, e2e, r.grid.current.numel()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_e2e_at_two_ranks(ref_fields):
+    """bench.py's N>1 end-to-end leg: every step re-uploads the slab and reruns the sweeps."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_e2e_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    full, e2e, n = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ref = ref_fields["dist_P2_h4_s2"]            # 8 levels from the initial field
+    assert np.array_equal(full.view(np.uint64), ref.view(np.uint64))
+    assert e2e["ms_per_step"] > 0 and e2e["unit"] == "GLUP/s"
+    assert e2e["h2d_bytes_per_step"] == 2 * n * 8
+    assert e2e["d2h_bytes_per_step"] == 2 * 20 * 10 * 12 * 8
