@@ -205,6 +205,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--transport", choices=("p2p", "nccl"), default="p2p",
+                    help="N>1 halo exchange: p2p = boundary kernels store into the neighbours' "
+                         "grids (CUDA IPC, NVLink), nccl = NCCL send/recv of the planes")
     ap.add_argument("--slab-runner", action="store_true",
                     help="dev: use the multi-GPU SlabRunner path even at N=1 (run under torchrun)")
     args = ap.parse_args()
@@ -268,8 +271,16 @@ def main():
                     pass_events.append((t, e0, e1))
     else:
         from paper_0912_4506_b200.dist import SlabRunner
-        runner = SlabRunner(sp.GridDims(nx, ny, nz * world), pat, h=T, dtype=dtype, device=dev,
-                            depth=T)
+        transport = args.transport if world > 1 else "nccl"
+        try:
+            runner = SlabRunner(sp.GridDims(nx, ny, nz * world), pat, h=T, dtype=dtype, device=dev,
+                                depth=T, transport=transport)
+        except Exception as exc:          # p2p mapping refused (no peer access): NCCL planes
+            if transport != "p2p":
+                raise
+            transport = f"nccl (p2p setup failed: {type(exc).__name__}: {exc})"[:200]
+            runner = SlabRunner(sp.GridDims(nx, ny, nz * world), pat, h=T, dtype=dtype, device=dev,
+                                depth=T, transport="nccl")
         grid = runner.grid
 
         def step(record=False):
@@ -363,6 +374,7 @@ def main():
             "config": {"workload": desc, "T": T, "passes_per_step": len(passes),
                        "global_interior_zyx": list(gshape), "per_gpu_interior_zyx": list(shape),
                        "parallelism": f"zslab{world}", "variant": args.variant or "auto",
+                       "halo_transport": transport if use_runner else None,
                        "l2": "inputs larger than L2 (one grid = %.1f GB >> 126 MB)" % (
                            grid.buffers[0].numel() * es / 1e9)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -382,6 +394,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
+        if use_runner:
+            runner.close()
         dist.barrier()
         dist.destroy_process_group()
     return 0
@@ -405,6 +419,7 @@ def measure_e2e_dist(torch, dist, runner, passes, dev, world, steps=3):
         g.active = 0
         g.current.copy_(host_in, non_blocking=True)          # H2D
         g.other.copy_(g.current, non_blocking=True)          # B = copy of A (R/grid.py:132-133)
+        runner.sync_start()     # every rank's upload lands before a neighbour stores into it
         for t in passes:
             runner.step(levels=t)
         runner.finish()

@@ -108,6 +108,31 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
                      const int32_t ext_hi[3], const int64_t out_lo[3],
                      const int64_t out_hi[3], void* stream);
 
+/* sp_sweep_tb_part that also delivers its z-boundary planes to the z-slab
+ * neighbours (fused halo exchange over peer memory; replaces the send half of
+ * exchange_halos, R/decomp.py:149-179, for layouts (1,1,P)): every level-T
+ * output plane z < halo is stored a second time into peer_lo -- the
+ * allocation base of the z- neighbour's destination grid, which has this
+ * grid's layout except nz -- at its plane z + peer_lo_shift (= its nz), and
+ * every plane z >= nz - halo into peer_hi at plane z + peer_hi_shift
+ * (= -nz).  The pointers must be addressable from this device (CUDA IPC /
+ * peer access); a null pointer skips that side.  Ordering against the
+ * neighbours' own passes is the caller's (SlabRunner: one token per step). */
+int sp_sweep_tb_part_peer(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+                          const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+                          const int32_t ext_hi[3], const int64_t out_lo[3],
+                          const int64_t out_hi[3], void* peer_lo, int64_t peer_lo_shift,
+                          void* peer_hi, int64_t peer_hi_shift, int64_t halo, void* stream);
+
+/* Cross-process grid mapping for sp_sweep_tb_part_peer (CUDA IPC).
+ * sp_ipc_export: 64-byte handle of the device allocation holding ptr and
+ * ptr's byte offset inside it.  sp_ipc_import (another process): map it into
+ * the current device (peer access to the owner's GPU enabled on demand) and
+ * return the address of the exported byte.  sp_ipc_close unmaps. */
+int sp_ipc_export(const void* ptr, unsigned char handle[64], int64_t* offset);
+int sp_ipc_import(const unsigned char handle[64], int64_t offset, void** ptr);
+int sp_ipc_close(void* ptr, int64_t offset);
+
 /* `levels` full-interior sweeps as passes of depth T (last pass shorter),
  * ping-ponging a/b.  *active: in = which array holds the current level
  * (0 = a), out = which holds the result (TwoGrid.active, R/grid.py:136-149).

@@ -34,8 +34,9 @@ NVCC_FLAGS = [
 
 # Symbols include/stencilpipe_b200.h declares (checked by the CPU tests).
 EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "sp_fill",
-           "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_run_sweeps",
-           "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule")
+           "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_sweep_tb_part_peer", "sp_run_sweeps",
+           "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule", "sp_ipc_export",
+           "sp_ipc_import", "sp_ipc_close")
 
 
 class NativeUnavailable(RuntimeError):
@@ -109,6 +110,14 @@ def load_library():
                               i32p, i32p, vp]
     L.sp_sweep_tb_part.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int, i64p, i64p,
                                    i32p, i32p, i64p, i64p, vp]
+    if hasattr(L, "sp_sweep_tb_part_peer") or not override:
+        L.sp_sweep_tb_part_peer.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int, i64p, i64p,
+                                            i32p, i32p, i64p, i64p, vp, ctypes.c_int64, vp,
+                                            ctypes.c_int64, ctypes.c_int64, vp]
+    if hasattr(L, "sp_ipc_export") or not override:
+        L.sp_ipc_export.argtypes = [vp, P(ctypes.c_ubyte * 64), P(ctypes.c_int64)]
+        L.sp_ipc_import.argtypes = [P(ctypes.c_ubyte * 64), ctypes.c_int64, P(vp)]
+        L.sp_ipc_close.argtypes = [vp, ctypes.c_int64]
     L.sp_run_sweeps.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int64, ctypes.c_int,
                                 P(ctypes.c_int), vp]
     L.sp_digest.argtypes = [vp, ctypes.c_int, P(Layout), ctypes.c_int64, P(ctypes.c_uint64), vp]

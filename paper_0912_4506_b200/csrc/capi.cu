@@ -9,6 +9,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdint>
+#include <cstring>
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
@@ -237,7 +239,7 @@ int variant_for(int dtype, int T) {
     return ok ? v : 0;
 }
 
-template <typename R, int T, int V>
+template <typename R, int T, int V, bool PEER = false>
 int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
                 cudaStream_t stream) {
     if constexpr (!usable<R, T, V>()) {
@@ -245,7 +247,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
     } else {
         constexpr Variant v = kVariants[V];
         using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split>;
+        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER>;
         const size_t smem = Pl::SMEM;
         // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
         static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
@@ -316,6 +318,39 @@ int launch_tb(int T, int v, const void* src, const sp_layout* L, const sp::TBArg
     }
 }
 
+// Peer-store launches (boundary slabs of a z-slab rank) use the fallback
+// variant 0 only: they cover h planes, a small share of a step.
+constexpr int kPeerVariant = 0;
+
+template <typename R>
+int launch_tb_peer(int T, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
+                   cudaStream_t s) {
+    switch (T) {
+        case 1: return launch_tb_t<R, 1, kPeerVariant, true>(src, L, a, grid, s);
+        case 2: return launch_tb_t<R, 2, kPeerVariant, true>(src, L, a, grid, s);
+        case 3: return launch_tb_t<R, 3, kPeerVariant, true>(src, L, a, grid, s);
+        case 4: return launch_tb_t<R, 4, kPeerVariant, true>(src, L, a, grid, s);
+        case 5: return launch_tb_t<R, 5, kPeerVariant, true>(src, L, a, grid, s);
+        case 6: return launch_tb_t<R, 6, kPeerVariant, true>(src, L, a, grid, s);
+        case 7: return launch_tb_t<R, 7, kPeerVariant, true>(src, L, a, grid, s);
+        case 8: return launch_tb_t<R, 8, kPeerVariant, true>(src, L, a, grid, s);
+        default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
+    }
+}
+
+struct PeerArgs {
+    void* lo;          // allocation base of the z- neighbour's destination grid (or null)
+    int64_t lo_shift;  // my plane z -> its plane z + lo_shift
+    void* hi;
+    int64_t hi_shift;
+    int64_t halo;      // planes [0, halo) go to lo, [nz - halo, nz) to hi
+};
+
+int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+               const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+               const int32_t ext_hi[3], const int64_t out_lo[3], const int64_t out_hi[3],
+               const PeerArgs* peer, void* stream);
+
 }  // namespace
 
 extern "C" {
@@ -333,6 +368,49 @@ int sp_set_tuning(int variant, int chunks) {
     g_use_k1 = variant < 0 ? 1 : 0;   // variant -1: K1 for single-level sweeps
     if (variant < 0) g_variant_override = -1;
     return prev;
+}
+
+int sp_ipc_export(const void* ptr, unsigned char handle[64], int64_t* offset) {
+    if (!ptr || !handle || !offset) return fail(SP_ERR_ARG, "null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    // the caching allocator sub-allocates: the handle names the whole cudaMalloc block
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range_fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            range_fn = reinterpret_cast<RangeFn>(p);
+    });
+    if (!range_fn) return fail(SP_ERR_DEVICE, "cuMemGetAddressRange unavailable");
+    if (range_fn(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+        return fail(SP_ERR_DEVICE, "cuMemGetAddressRange failed for %p", ptr);
+    cudaIpcMemHandle_t h;
+    SP_CUDA(cudaIpcGetMemHandle(&h, (void*)base));
+    std::memcpy(handle, &h, 64);
+    *offset = (int64_t)((CUdeviceptr)ptr - base);
+    return SP_OK;
+}
+
+int sp_ipc_import(const unsigned char handle[64], int64_t offset, void** ptr) {
+    if (!handle || !ptr) return fail(SP_ERR_ARG, "null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, 64);
+    void* base = nullptr;
+    // mapped into the current device; peer access to the owner's device is enabled lazily
+    SP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr = (char*)base + offset;
+    return SP_OK;
+}
+
+int sp_ipc_close(void* ptr, int64_t offset) {
+    if (!ptr) return SP_OK;
+    SP_CUDA(cudaIpcCloseMemHandle((char*)ptr - offset));
+    return SP_OK;
 }
 
 int sp_set_schedule(int dynamic, int strip) {
@@ -388,6 +466,28 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
                      const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
                      const int32_t ext_hi[3], const int64_t out_lo[3], const int64_t out_hi[3],
                      void* stream) {
+    return sweep_part(src, dst, dtype, L, T, lo, hi, ext_lo, ext_hi, out_lo, out_hi, nullptr, stream);
+}
+
+int sp_sweep_tb_part_peer(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+                          const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+                          const int32_t ext_hi[3], const int64_t out_lo[3], const int64_t out_hi[3],
+                          void* peer_lo, int64_t peer_lo_shift, void* peer_hi, int64_t peer_hi_shift,
+                          int64_t halo, void* stream) {
+    if (halo < 1 || (peer_lo == nullptr && peer_hi == nullptr))
+        return fail(SP_ERR_ARG, "peer pass needs halo >= 1 and at least one neighbour grid");
+    PeerArgs p{peer_lo, peer_lo_shift, peer_hi, peer_hi_shift, halo};
+    return sweep_part(src, dst, dtype, L, T, lo, hi, ext_lo, ext_hi, out_lo, out_hi, &p, stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
+               const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
+               const int32_t ext_hi[3], const int64_t out_lo[3], const int64_t out_hi[3],
+               const PeerArgs* peer, void* stream) {
     int rc = check_layout(L, dtype);
     if (rc) return rc;
     if (!src || !dst || !lo || !hi || !out_lo || !out_hi) return fail(SP_ERR_ARG, "null argument");
@@ -434,7 +534,7 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
         a.ox = ((sp::WX - 2 * T) / A) * A;
     else
         a.ox = sp::WX - 2 * T - (A - 1);
-    const int variant = variant_for(dtype, T);
+    const int variant = peer ? kPeerVariant : variant_for(dtype, T);
     const int wy = kVariants[variant].by * kVariants[variant].py;
     if (wy - 2 * T < 1) return fail(SP_ERR_SCHEDULE, "depth T=%d too deep for a %d-row footprint", T, wy);
     a.oy = wy - 2 * T;
@@ -472,9 +572,39 @@ int sp_sweep_tb_part(const void* src, void* dst, int dtype, const sp_layout* L, 
     }
     int grid = (int)std::min<int64_t>(a.units, slots);
     cudaStream_t s = (cudaStream_t)stream;
+    a.rd_lo = a.rd_hi = 0;
+    a.rz_lo = INT32_MIN;
+    a.rz_hi = INT32_MAX;
+    if (peer) {
+        // neighbours share this layout (same nx, ny, ghosts; only nz differs), so a
+        // plane's copy sits a fixed element offset away in the neighbour's grid
+        const int64_t es = elem_size(dtype);
+        auto delta = [&](void* base, int64_t shift) {
+            const int64_t bytes = (int64_t)((intptr_t)base - (intptr_t)dst);
+            return bytes / es + shift * L->pz;
+        };
+        if (peer->lo) {
+            if (((intptr_t)peer->lo - (intptr_t)dst) % 16 != 0)
+                return fail(SP_ERR_ARG, "neighbour grid is not 16-byte aligned with this one");
+            a.rd_lo = delta(peer->lo, peer->lo_shift);
+            a.rz_lo = (int)peer->halo;
+        }
+        if (peer->hi) {
+            if (((intptr_t)peer->hi - (intptr_t)dst) % 16 != 0)
+                return fail(SP_ERR_ARG, "neighbour grid is not 16-byte aligned with this one");
+            a.rd_hi = delta(peer->hi, peer->hi_shift);
+            a.rz_hi = (int)(L->nz - peer->halo);
+        }
+        if (dtype == SP_F64) return launch_tb_peer<double>(T, src, L, a, grid, s);
+        return launch_tb_peer<float>(T, src, L, a, grid, s);
+    }
     if (dtype == SP_F64) return launch_tb<double>(T, variant, src, L, a, grid, s);
     return launch_tb<float>(T, variant, src, L, a, grid, s);
 }
+
+}  // namespace
+
+extern "C" {
 
 int sp_sweep_tb(const void* src, void* dst, int dtype, const sp_layout* L, int T,
                 const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],

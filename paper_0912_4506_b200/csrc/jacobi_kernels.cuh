@@ -48,6 +48,11 @@ struct TBArgs {
     int align;                 // elements per 16 bytes (TMA box start alignment)
     unsigned* sched;           // unit counter (dynamic schedule; zero on entry and exit) or null
     int strip;                 // unit order: tile-column strips of this width, y-major (0: x-major)
+    // PEER launches: level-T planes p < rz_lo are stored a second time at
+    // (address + rd_lo) -- the z- neighbour's ghost planes, peer memory over
+    // NVLink -- and planes p >= rz_hi at (address + rd_hi) for the z+ one.
+    int64_t rd_lo, rd_hi;      // element offsets from this grid to the neighbours' planes
+    int rz_lo, rz_hi;
 };
 
 // ---- small PTX helpers ------------------------------------------------------
@@ -177,7 +182,8 @@ struct Plan {
     static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + (RING + 2) * 8 + NUID * 4;
 };
 
-template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV>
+template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV,
+          bool PEER = false>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
@@ -481,18 +487,26 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             // and the tuned variant table picks per (dtype, T).
             if (st >= 2 * T) {
                 R* d = RSTORE ? dnext : dcol + (int64_t)(q - T) * pz;
-                if (vec_store) {
+                auto put = [&](R* b) {
+                    if (vec_store) {
 #pragma unroll
-                    for (int j = 0; j < PY; ++j)
-                        if ((wyb >> j) & 1u)
-                            __stcs(reinterpret_cast<V2*>(d + j * py), V2{out[j][0], out[j][1]});
-                } else {
+                        for (int j = 0; j < PY; ++j)
+                            if ((wyb >> j) & 1u)
+                                __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < PY; ++j) {
-                        const bool row = (wyb >> j) & 1u;
-                        if (row && (wx & 1u)) __stcs(d + j * py, out[j][0]);
-                        if (row && (wx & 2u)) __stcs(d + j * py + 1, out[j][1]);
+                        for (int j = 0; j < PY; ++j) {
+                            const bool row = (wyb >> j) & 1u;
+                            if (row && (wx & 1u)) __stcs(b + j * py, out[j][0]);
+                            if (row && (wx & 2u)) __stcs(b + j * py + 1, out[j][1]);
+                        }
                     }
+                };
+                put(d);
+                if constexpr (PEER) {   // the same plane into a neighbour's ghost plane
+                    const int p = q - T;
+                    if (p < a.rz_lo) put(d + a.rd_lo);
+                    if (p >= a.rz_hi) put(d + a.rd_hi);
                 }
             }
             if (RSTORE) dnext += pz;

@@ -16,6 +16,18 @@ The interior slab needs no ghost plane (its level-1 reads stay inside
 alternates exchange and compute strictly; results are
 bit-identical either way because the per-cell arithmetic is unchanged.
 
+``transport="p2p"`` fuses the exchange into the boundary kernels: each rank
+maps its z-neighbours' grids (CUDA IPC through torch's tensor sharing) and
+the boundary K2 launches store their level-T planes a second time straight
+into the neighbours' ghost planes over NVLink (sp_sweep_tb_part_peer).  Only
+a one-element token per neighbour and step travels through the process group:
+
+  step k:  wait for the neighbours' tokens of step k-1    (their planes have
+           landed in my ghosts, and they finished reading the ghosts I write)
+           boundary K2 -> my S_{k+1} planes + the neighbours' S_{k+1} ghosts
+           send my step-k token                            (after the kernels)
+           interior K2
+
 ``engine`` abstracts the grid + pass implementation so the exchange logic is
 testable on CPU with gloo (tests supply a host engine); the default is the
 CUDA engine and there is no fallback.
@@ -42,6 +54,55 @@ class CudaEngine:
         from .pipeline import run_pass
         run_pass(grid, T, lo, hi, e_lo, e_hi, out_lo=out_lo, out_hi=out_hi)
 
+    def run_pass_peer(self, grid, T, lo, hi, e_lo, e_hi, out_lo, out_hi, peer):
+        from .pipeline import run_pass
+        run_pass(grid, T, lo, hi, e_lo, e_hi, out_lo=out_lo, out_hi=out_hi, peer=peer)
+
+    def sync(self, grid):
+        import torch
+        torch.cuda.current_stream(grid.device).synchronize()
+
+    def share(self, grid):
+        """CUDA IPC handles of both grids (picklable)."""
+        import ctypes
+        from . import _native as N
+        out = []
+        for b in grid.buffers:
+            h, off = (ctypes.c_ubyte * 64)(), ctypes.c_int64()
+            N.check(N.lib().sp_ipc_export(ctypes.c_void_p(b.data_ptr()), ctypes.byref(h), ctypes.byref(off)))
+            out.append((bytes(h), off.value))
+        return out
+
+    def open(self, grid, shared):
+        """Map a neighbour's grids into this rank's device."""
+        import ctypes
+        import torch
+        from . import _native as N
+        bufs = []
+        with torch.cuda.device(grid.device):
+            for h, off in shared:
+                ptr = ctypes.c_void_p()
+                N.check(N.lib().sp_ipc_import(ctypes.byref((ctypes.c_ubyte * 64).from_buffer_copy(h)),
+                                              off, ctypes.byref(ptr)))
+                bufs.append(PeerBuffer(ptr.value, off))
+        return bufs
+
+    def close(self, grid, bufs):
+        from . import _native as N
+        for b in bufs:
+            N.check(N.lib().sp_ipc_close(b.ptr, b.offset))
+
+
+class PeerBuffer:
+    """A neighbour's grid allocation mapped into this process (CUDA IPC)."""
+
+    def __init__(self, ptr: int, offset: int):
+        self.ptr = ptr
+        self.offset = offset
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
     def default_depth(self, grid):
         return DEFAULT_DEPTH[grid.sp_dtype]
 
@@ -51,7 +112,7 @@ class SlabRunner:
 
     def __init__(self, global_dims: GridDims, pattern, h: int, dtype=np.float64,
                  depth: int | None = None, device=None, engine=None, overlap: bool = True,
-                 group=None):
+                 group=None, transport: str = "nccl"):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
@@ -72,6 +133,101 @@ class SlabRunner:
         self._primed = False
         self.messages = 0
         self.bytes_sent = 0
+        if transport not in ("nccl", "p2p"):
+            raise DecompositionError(f"unknown halo transport {transport!r}")
+        self.transport = transport
+        if transport == "p2p":
+            if not self.overlap:
+                raise DecompositionError("p2p halos need one pass per step (h <= depth) and nz > 2h")
+            self._map_peers()
+
+    # -- p2p transport -------------------------------------------------------
+
+    def _map_peers(self):
+        """Map both grids of each z-neighbour into this process (the engine's
+        IPC: CUDA IPC handles for device grids, shared memory for the host
+        test engine)."""
+        import torch
+        dist = self.dist
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, self.engine.share(self.grid), group=self.group)
+        self._peer = {}
+        err = None
+        try:
+            for nb in (self.lo_nb, self.hi_nb):
+                if nb is not None:
+                    self._peer[nb] = self.engine.open(self.grid, everyone[nb])
+        except Exception as exc:      # decided collectively below, so every rank agrees
+            err = exc
+        ok = torch.tensor([0 if err else 1], dtype=torch.int32,
+                          device=None if dist.get_backend(self.group) != "nccl" else self.grid.buffers[0].device)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=self.group)
+        if not int(ok.item()):
+            for bufs in self._peer.values():
+                self.engine.close(self.grid, bufs)
+            self._peer = {}
+            raise DecompositionError(f"p2p mapping failed on some rank: {err or 'see that rank'}")
+        self._nz = [self.decomp.local_dims(r).nz for r in range(self.world)]
+        self._host_tokens = dist.get_backend(self.group) != "nccl"
+        dev = None if self._host_tokens else self.grid.buffers[0].device
+        self._tok_out = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._tok_in = {nb: torch.zeros(1, dtype=torch.int32, device=dev) for nb in self._peer}
+        self.sync_start()
+
+    def close(self):
+        """Unmap the neighbours' grids (p2p transport)."""
+        self.finish()
+        if getattr(self, "_peer", None):
+            self.engine.sync(self.grid)
+            self.dist.barrier(group=self.group)      # nobody stores into a grid being unmapped
+            for bufs in self._peer.values():
+                self.engine.close(self.grid, bufs)
+            self._peer = {}
+
+    def sync_start(self):
+        """All ranks' grids are written (fill / upload) before anyone's next step
+        may store into them; a no-op ordering point for the NCCL transport."""
+        self.finish()
+        self.engine.sync(self.grid)
+        self.dist.barrier(group=self.group)
+
+    def _peer_args(self):
+        """(lo_buf, lo_shift, hi_buf, hi_shift, h) for the destination grid of this step."""
+        k = 1 - self.grid.active          # ranks swap in lockstep: same buffer index
+        lo = self._peer[self.lo_nb][k] if self.lo_nb is not None else None
+        hi = self._peer[self.hi_nb][k] if self.hi_nb is not None else None
+        lo_shift = self._nz[self.lo_nb] if self.lo_nb is not None else 0
+        return lo, lo_shift, hi, -self.grid.dims.nz, self.h
+
+    def _signal(self):
+        """Send this step's token to both neighbours, post receives of theirs."""
+        dist = self.dist
+        if self._host_tokens:
+            self.engine.sync(self.grid)   # host-delivered token: the peer stores are done
+        ops = []
+        for nb in (self.lo_nb, self.hi_nb):
+            if nb is None:
+                continue
+            ops.append(dist.P2POp(dist.isend, self._tok_out, self._global_rank(nb), self.group))
+            ops.append(dist.P2POp(dist.irecv, self._tok_in[nb], self._global_rank(nb), self.group))
+        if ops:
+            self._pending.extend(dist.batch_isend_irecv(ops))
+            self.messages += len(ops) // 2
+
+    def _step_p2p(self, r):
+        g, h = self.grid, self.h
+        self._wait()
+        lo, hi = self._domain(r, 0, r)
+        nz = g.dims.nz
+        low = ((0, lo[1], lo[2]), (h, hi[1], hi[2]))
+        high = ((nz - h, lo[1], lo[2]), (nz, hi[1], hi[2]))
+        inner = ((h, lo[1], lo[2]), (nz - h, hi[1], hi[2]))
+        peer = self._peer_args()
+        for olo, ohi in (low, high):
+            self.engine.run_pass_peer(g, r, lo, hi, self.e_lo, self.e_hi, olo, ohi, peer)
+        self._signal()
+        self.engine.run_pass(g, r, lo, hi, self.e_lo, self.e_hi, *inner)
+        g.swap()
 
     # -- halo exchange ---------------------------------------------------------
 
@@ -126,6 +282,8 @@ class SlabRunner:
         r = h if levels is None else int(levels)
         if not 1 <= r <= h:
             raise DecompositionError(f"step of {r} levels needs 1 <= levels <= h={h}")
+        if self.transport == "p2p":
+            return self._step_p2p(r)
         if not self.overlap or r > self.depth:
             if self._primed:
                 self._wait()
@@ -184,3 +342,46 @@ class SlabRunner:
 def check_layout(layout):
     if tuple(layout[:2]) != (1, 1):
         raise DecompositionError("SlabRunner decomposes in z only: layout (1, 1, P)")
+
+
+def emulate_peer_slabs(global_dims: GridDims, pattern, ranks: int, h: int, levels, dtype=np.float64,
+                       device=None):
+    """Single-device emulation of the p2p transport: ``ranks`` z-slab grids in
+    this process, each step's boundary launches storing straight into the
+    neighbour slabs' ghost planes (the pointers a multi-GPU run maps through
+    IPC), then the interior launches; one stream orders everything, which is
+    what the per-step tokens guarantee across processes.  Returns the
+    gathered global interior (numpy)."""
+    from .decomp import local_grid
+    from .pipeline import run_pass
+    decomp = decompose(global_dims, ranks, (1, 1, ranks), h)
+    grids = [local_grid(decomp, r, pattern, dtype=dtype, device=device) for r in range(ranks)]
+    flags = [face_flags(decomp, r) for r in range(ranks)]
+    nbs = [(decomp.neighbor(r, 0, high=False), decomp.neighbor(r, 0, high=True)) for r in range(ranks)]
+    for lv in levels:
+        if not 1 <= lv <= h:
+            raise DecompositionError(f"step of {lv} levels needs 1 <= levels <= h={h}")
+        inner_jobs = []
+        for r, g in enumerate(grids):
+            e_lo, e_hi = flags[r]
+            shape = g.dims.shape
+            lo, hi = (0, 0, 0), tuple(shape)
+            nz = g.dims.nz
+            lo_nb, hi_nb = nbs[r]
+            k = 1 - g.active
+            peer = (grids[lo_nb].buffers[k] if lo_nb is not None else None,
+                    grids[lo_nb].dims.nz if lo_nb is not None else 0,
+                    grids[hi_nb].buffers[k] if hi_nb is not None else None, -nz, h)
+            for olo, ohi in (((0, 0, 0), (h, shape[1], shape[2])),
+                             ((nz - h, 0, 0), (nz, shape[1], shape[2]))):
+                run_pass(g, lv, lo, hi, e_lo, e_hi, out_lo=olo, out_hi=ohi, peer=peer)
+            inner_jobs.append((g, lv, lo, hi, e_lo, e_hi, (h, 0, 0), (nz - h, shape[1], shape[2])))
+        for g, lv, lo, hi, e_lo, e_hi, olo, ohi in inner_jobs:
+            run_pass(g, lv, lo, hi, e_lo, e_hi, out_lo=olo, out_hi=ohi)
+        for g in grids:
+            g.swap()
+    full = np.empty(decomp.global_dims.shape, dtype=grids[0].dtype)
+    for r, g in enumerate(grids):
+        sl = tuple(slice(a, b) for a, b in decomp.ranges(r))
+        full[sl] = g.interior()
+    return full

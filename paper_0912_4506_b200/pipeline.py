@@ -154,13 +154,30 @@ def domains_to_passes(level_domains, U: int, depth: int):
 
 
 def run_pass(grid: TwoGrid, T: int, lo, hi, e_lo=(0, 0, 0), e_hi=(0, 0, 0),
-             out_lo=None, out_hi=None, src=None, dst=None, stream=None) -> None:
-    """One K2 launch: T levels from ``src`` (default current) into ``dst``."""
+             out_lo=None, out_hi=None, src=None, dst=None, stream=None, peer=None) -> None:
+    """One K2 launch: T levels from ``src`` (default current) into ``dst``.
+
+    ``peer = (lo_buf, lo_shift, hi_buf, hi_shift, halo)``: also store output
+    planes z < halo into ``lo_buf`` at plane z + lo_shift and planes
+    z >= nz - halo into ``hi_buf`` at z + hi_shift (device buffers of the
+    z-neighbours' destination grids, same layout; None skips a side).
+    """
     src = grid.current_buffer() if src is None else src
     dst = grid.other_buffer() if dst is None else dst
     s = grid.stream() if stream is None else ctypes.c_void_p(stream)
     with _on(grid.device):
-        if out_lo is None:
+        if peer is not None:
+            b_lo, s_lo, b_hi, s_hi, halo = peer
+            o_lo = lo if out_lo is None else out_lo
+            o_hi = hi if out_hi is None else out_hi
+            N.check(N.lib().sp_sweep_tb_part_peer(
+                ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), grid.sp_dtype,
+                ctypes.byref(grid.layout), int(T), N.i64x3(lo), N.i64x3(hi), N.i32x3(e_lo),
+                N.i32x3(e_hi), N.i64x3(o_lo), N.i64x3(o_hi),
+                ctypes.c_void_p(b_lo.data_ptr() if b_lo is not None else None), int(s_lo),
+                ctypes.c_void_p(b_hi.data_ptr() if b_hi is not None else None), int(s_hi),
+                int(halo), s))
+        elif out_lo is None:
             N.check(N.lib().sp_sweep_tb(
                 ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), grid.sp_dtype,
                 ctypes.byref(grid.layout), int(T), N.i64x3(lo), N.i64x3(hi), N.i32x3(e_lo),

@@ -30,14 +30,19 @@ class HostGrid:
         self.dims = dims
         self.dtype = dtype
         td = torch.float64 if dtype == np.float64 else torch.float32
-        self._a = torch.zeros(n.value, dtype=td)
-        self._b = torch.zeros(n.value, dtype=td)
+        # shared memory, so the p2p transport can map a neighbour's grids
+        self._a = torch.zeros(n.value, dtype=td).share_memory_()
+        self._b = torch.zeros(n.value, dtype=td).share_memory_()
         olay = O._Layout(*lay.as_tuple())
         self.olay = olay
         fill = O.lib().or_fill_f64 if dtype == np.float64 else O.lib().or_fill_f32
         fill(self._a.data_ptr(), ctypes.byref(olay), ctypes.byref(O._c_pattern(pattern)))
         self._b.copy_(self._a)
         self.active = 0
+
+    @property
+    def buffers(self):
+        return (self._a, self._b)
 
     @property
     def torch_dtype(self):
@@ -105,3 +110,38 @@ class HostEngine:
             for y in range(out_lo[1], out_hi[1]):
                 o = lay.origin + z * lay.pz + y * lay.py
                 dst[o + out_lo[2]:o + out_hi[2]] = res[o + out_lo[2]:o + out_hi[2]]
+
+    def run_pass_peer(self, g, T, lo, hi, e_lo, e_hi, out_lo, out_hi, peer):
+        """run_pass, then the kernel's peer stores: output planes z < halo into
+        the z- neighbour's grid at z + lo_shift, z >= nz - halo into the z+ one."""
+        self.run_pass(g, T, lo, hi, e_lo, e_hi, out_lo, out_hi)
+        b_lo, s_lo, b_hi, s_hi, halo = peer
+        dst = g.other_buffer()
+        lay = g.layout
+        for z in range(out_lo[0], out_hi[0]):
+            for buf, shift, take in ((b_lo, s_lo, z < halo), (b_hi, s_hi, z >= lay.nz - halo)):
+                if buf is None or not take:
+                    continue
+                for y in range(out_lo[1], out_hi[1]):
+                    o = lay.origin + z * lay.pz + y * lay.py
+                    r = o + shift * lay.pz
+                    buf[r + out_lo[2]:r + out_hi[2]] = dst[o + out_lo[2]:o + out_hi[2]]
+
+    def sync(self, g):
+        pass
+
+    def share(self, g):
+        import io
+        import pickle
+        from multiprocessing.reduction import ForkingPickler
+        import torch.multiprocessing  # noqa: F401  (registers the tensor reducers)
+        blob = io.BytesIO()
+        ForkingPickler(blob, pickle.HIGHEST_PROTOCOL).dump(list(g.buffers))
+        return blob.getvalue()
+
+    def open(self, g, shared):
+        import pickle
+        return pickle.loads(shared)
+
+    def close(self, g, bufs):
+        pass

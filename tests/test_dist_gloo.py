@@ -24,7 +24,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, h, steps, overlap, levels, q):
+def _worker(rank, world, port, h, steps, overlap, levels, q, transport="nccl"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -36,12 +36,14 @@ def _worker(rank, world, port, h, steps, overlap, levels, q):
     import paper_0912_4506_b200 as sp
     from paper_0912_4506_b200.dist import SlabRunner
 
+    import torch.multiprocessing as tmp
+    tmp.set_sharing_strategy("file_system")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         gshape = (40, 10, 12)
         base = O.BoxPattern("random", seed=0, faces=Z1, global_shape=gshape)
         r = SlabRunner(sp.GridDims(12, 10, 40), None, h=h, dtype=np.float64, depth=h,
-                       engine=HostEngine(base), overlap=overlap)
+                       engine=HostEngine(base), overlap=overlap, transport=transport)
         for lv in levels or [h] * steps:
             r.step(levels=lv)
         r.finish()
@@ -52,11 +54,11 @@ def _worker(rank, world, port, h, steps, overlap, levels, q):
         dist.destroy_process_group()
 
 
-def _run(world, h, steps, overlap=True, levels=None):
+def _run(world, h, steps, overlap=True, levels=None, transport="nccl"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, h, steps, overlap, levels, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, h, steps, overlap, levels, q, transport))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -86,7 +88,7 @@ def test_three_ranks_with_remainder_step(O):
     assert np.array_equal(full.view(np.uint64), g.interior().view(np.uint64))
 
 
-def _e2e_worker(rank, world, port, q):
+def _e2e_worker(rank, world, port, q, transport="nccl"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -100,12 +102,14 @@ def _e2e_worker(rank, world, port, q):
     import paper_0912_4506_b200 as sp
     from paper_0912_4506_b200.dist import SlabRunner
 
+    import torch.multiprocessing as tmp
+    tmp.set_sharing_strategy("file_system")
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         gshape = (40, 10, 12)
         base = O.BoxPattern("random", seed=0, faces=Z1, global_shape=gshape)
         r = SlabRunner(sp.GridDims(12, 10, 40), None, h=4, dtype=np.float64, depth=4,
-                       engine=HostEngine(base))
+                       engine=HostEngine(base), transport=transport)
         e2e = bench.measure_e2e_dist(torch, dist, r, [4, 4], torch.device("cpu"), world, steps=2)
         full = r.gather()
         if rank == 0:
@@ -114,12 +118,13 @@ def _e2e_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_bench_e2e_at_two_ranks(ref_fields):
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_bench_e2e_at_two_ranks(ref_fields, transport):
     """bench.py's N>1 end-to-end leg: every step re-uploads the slab and reruns the sweeps."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_e2e_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_e2e_worker, args=(r, 2, port, q, transport)) for r in range(2)]
     for p in procs:
         p.start()
     full, e2e, n = q.get(timeout=120)
@@ -131,3 +136,14 @@ def test_bench_e2e_at_two_ranks(ref_fields):
     assert e2e["ms_per_step"] > 0 and e2e["unit"] == "GLUP/s"
     assert e2e["h2d_bytes_per_step"] == 2 * n * 8
     assert e2e["d2h_bytes_per_step"] == 2 * 20 * 10 * 12 * 8
+
+
+@pytest.mark.parametrize("world,h,levels", [(2, 4, [4, 4]), (3, 2, [2, 2, 1, 2]), (2, 1, [1, 1, 1])])
+def test_p2p_transport_peer_stores(O, world, h, levels):
+    """transport="p2p": boundary passes store into the mapped neighbour grids,
+    one token per neighbour and step; bit-identical to the undecomposed sweeps."""
+    full, did_overlap, msgs = _run(world, h, 0, True, levels=levels, transport="p2p")
+    g = O.CGrid((40, 10, 12), O.BoxPattern("random", seed=0, faces=Z1, global_shape=(40, 10, 12)))
+    g.sweeps(sum(levels))
+    assert np.array_equal(full.view(np.uint64), g.interior().view(np.uint64))
+    assert msgs > 0
