@@ -347,7 +347,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         if not use_runner:
-            e2e = measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=max(args.steps, 3))
+            # a stream of independent problems: >= 10 steps so the pipeline's fill
+            # (first upload) and drain (last download) are a small share
+            e2e = measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=max(args.steps, 10))
         else:
             e2e = measure_e2e_dist(torch, dist, runner, passes, dev, world, steps=max(args.steps, 3))
 
@@ -410,20 +412,27 @@ def measure_e2e_dist(torch, dist, runner, passes, dev, world, steps=3):
     host_in = torch.empty(tuple(g.current.shape), dtype=g.torch_dtype, pin_memory=cuda)
     host_in.copy_(g.current.cpu())                 # this rank's current field (untimed)
     host_out = torch.empty(tuple(g.dims.shape), dtype=g.torch_dtype, pin_memory=cuda)
+    upload = getattr(g, "upload", None)
 
     def sync():
         if cuda:
             torch.cuda.synchronize(dev)
 
     def one():
-        g.active = 0
-        g.current.copy_(host_in, non_blocking=True)          # H2D
-        g.other.copy_(g.current, non_blocking=True)          # B = copy of A (R/grid.py:132-133)
+        if upload is not None:
+            g.upload(host_in)                                # H2D + B = A (TwoGrid.upload)
+        else:                                                # host test engine
+            g.active = 0
+            g.current.copy_(host_in)
+            g.other.copy_(g.current)
         runner.sync_start()     # every rank's upload lands before a neighbour stores into it
         for t in passes:
             runner.step(levels=t)
         runner.finish()
-        host_out.copy_(g.interior_device(), non_blocking=True)   # D2H
+        if upload is not None:
+            g.download(host_out)                             # D2H (TwoGrid.download)
+        else:
+            host_out.copy_(g.interior_device())
 
     one()
     sync()
@@ -451,40 +460,40 @@ def measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=3):
 
     Every step uploads the ghosted initial field (dense (nz+2, ny+2, nx+2),
     as the reference's TwoGrid holds it) from pinned memory into a device
-    grid, runs the 100 sweeps, and reads the interior back into pinned
-    memory.  Steps are independent, so they are pipelined over two device
-    grids and three streams: upload k+1 | compute k | download k-1.
+    grid (TwoGrid.upload: one pitched DMA + the B = A device copy), runs the
+    100 sweeps, and reads the interior back into pinned memory
+    (TwoGrid.download, one pitched DMA).  Steps are independent, so they are
+    pipelined over three device grids and three streams -- upload k+1 |
+    compute k | download k-1 -- and the two PCIe directions run at once.
     """
     d = grid.dims
-    host_in = torch.empty(tuple(n + 2 for n in d.shape), dtype=grid.torch_dtype, pin_memory=True)
+    host_in = torch.empty(grid.host_shape(), dtype=grid.torch_dtype, pin_memory=True)
     host_in.copy_(grid.current.cpu())            # the initial field (untimed)
     host_out = [torch.empty(d.shape, dtype=grid.torch_dtype, pin_memory=True) for _ in range(2)]
-    grids = [grid, sp.TwoGrid(d, sp.FillPattern.constant(0.0), dtype=dtype, device=dev)]
+    grids = [grid] + [sp.TwoGrid(d, sp.FillPattern.constant(0.0), dtype=dtype, device=dev)
+                      for _ in range(2)]
     s_up, s_comp, s_down = (torch.cuda.Stream(dev) for _ in range(3))
     ev = lambda: torch.cuda.Event()                                      # noqa: E731
-    free = [ev(), ev()]
+    free = [ev() for _ in grids]
     sweeps_n = sum(passes)
     T = max(passes)
     for f in free:
         f.record(stream)
 
     def one(k):
-        g, i = grids[k % 2], k % 2
+        i = k % len(grids)
+        g = grids[i]
         loaded, done = ev(), ev()
-        with torch.cuda.stream(s_up):
-            s_up.wait_event(free[i])
-            g.active = 0
-            g.current.copy_(host_in, non_blocking=True)        # H2D
-            g.other.copy_(g.current, non_blocking=True)        # B = copy of A (R/grid.py:132-133)
-            loaded.record(s_up)
+        s_up.wait_event(free[i])
+        g.upload(host_in, stream=s_up.cuda_stream)                     # H2D
+        loaded.record(s_up)
         with torch.cuda.stream(s_comp):
             s_comp.wait_event(loaded)
-            sp.sweeps(g, sweeps_n, depth=T)                    # public API
+            sp.sweeps(g, sweeps_n, depth=T)                            # public API
             done.record(s_comp)
-        with torch.cuda.stream(s_down):
-            s_down.wait_event(done)
-            host_out[i].copy_(g.interior_device(), non_blocking=True)   # D2H
-            free[i].record(s_down)
+        s_down.wait_event(done)
+        g.download(host_out[k % 2], stream=s_down.cuda_stream)         # D2H
+        free[i].record(s_down)
 
     one(0)
     torch.cuda.synchronize(dev)
@@ -498,8 +507,8 @@ def measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=3):
     return {"value": round(lups / el / 1e9, 2), "unit": "GLUP/s",
             "h2d_bytes_per_step": host_in.numel() * es, "d2h_bytes_per_step": host_out[0].numel() * es,
             "steps": steps, "ms_per_step": round(el / steps * 1e3, 2),
-            "api": "TwoGrid.current.copy_(pinned) -> sweeps() -> interior_device() -> pinned; "
-                   "steps pipelined on 3 streams over 2 device grids"}
+            "api": "TwoGrid.upload(pinned) -> sweeps() -> TwoGrid.download(pinned); steps "
+                   "pipelined on 3 streams over 3 device grids"}
 
 
 if __name__ == "__main__":

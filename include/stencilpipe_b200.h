@@ -124,6 +124,20 @@ int sp_sweep_tb_part_peer(const void* src, void* dst, int dtype, const sp_layout
                           const int64_t out_hi[3], void* peer_lo, int64_t peer_lo_shift,
                           void* peer_hi, int64_t peer_hi_shift, int64_t halo, void* stream);
 
+/* Grid transfers (stream-ordered; host memory should be pinned for
+ * asynchrony).  sp_copy_in: the dense ghosted box (nz+2gz, ny+2gy, nx+2gx)
+ * -- the reference TwoGrid's array layout, R/grid.py:126-134 -- into the
+ * allocation at base_a and, if base_b is given, also base_b (B = copy of A,
+ * R/grid.py:132-133).  sp_copy_out: the interior (nz, ny, nx) of the
+ * allocation at base into dense host memory (TwoGrid.interior,
+ * R/grid.py:151-153).  With a device staging buffer (>= one plane) the data
+ * crosses PCIe as linear copies of whole planes, repacked on the device
+ * (K6); without one, as a single pitched 3-D DMA. */
+int sp_copy_in(const void* host, int dtype, const sp_layout* L, void* base_a, void* base_b,
+               void* staging, int64_t staging_elems, void* stream);
+int sp_copy_out(const void* base, int dtype, const sp_layout* L, void* host, void* staging,
+                int64_t staging_elems, void* stream);
+
 /* Cross-process grid mapping for sp_sweep_tb_part_peer (CUDA IPC).
  * sp_ipc_export: 64-byte handle of the device allocation holding ptr and
  * ptr's byte offset inside it.  sp_ipc_import (another process): map it into

@@ -36,7 +36,7 @@ NVCC_FLAGS = [
 EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "sp_fill",
            "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_sweep_tb_part_peer", "sp_run_sweeps",
            "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule", "sp_ipc_export",
-           "sp_ipc_import", "sp_ipc_close")
+           "sp_ipc_import", "sp_ipc_close", "sp_copy_in", "sp_copy_out")
 
 
 class NativeUnavailable(RuntimeError):
@@ -114,6 +114,9 @@ def load_library():
         L.sp_sweep_tb_part_peer.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int, i64p, i64p,
                                             i32p, i32p, i64p, i64p, vp, ctypes.c_int64, vp,
                                             ctypes.c_int64, ctypes.c_int64, vp]
+    if hasattr(L, "sp_copy_in") or not override:
+        L.sp_copy_in.argtypes = [vp, ctypes.c_int, P(Layout), vp, vp, vp, ctypes.c_int64, vp]
+        L.sp_copy_out.argtypes = [vp, ctypes.c_int, P(Layout), vp, vp, ctypes.c_int64, vp]
     if hasattr(L, "sp_ipc_export") or not override:
         L.sp_ipc_export.argtypes = [vp, P(ctypes.c_ubyte * 64), P(ctypes.c_int64)]
         L.sp_ipc_import.argtypes = [P(ctypes.c_ubyte * 64), ctypes.c_int64, P(vp)]

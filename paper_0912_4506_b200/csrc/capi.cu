@@ -370,6 +370,111 @@ int sp_set_tuning(int variant, int chunks) {
     return prev;
 }
 
+// Host <-> device transfers of a grid.  With a staging buffer: linear
+// PCIe copies of whole dense planes through it, each followed by a K6
+// repack into the padded layout (linear DMA keeps both PCIe directions at
+// full rate when they run at once; pitched DMA of 8 KB rows does not).
+// Without: one pitched 3-D DMA.
+}  // extern "C"
+
+namespace {
+
+template <typename R>
+int row_copy(const void* src, void* dst, void* dst2, const sp::RowCopy& c, cudaStream_t s) {
+    DevInfo di;
+    int rc = dev_info(&di);
+    if (rc) return rc;
+    const int64_t rows = c.nz * c.ny;
+    const int grid = (int)std::min<int64_t>(rows, (int64_t)di.sms * 8);
+    sp::row_copy_kernel<R><<<grid, 256, 0, s>>>((const R*)src, (R*)dst, (R*)dst2, c);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "row_copy_kernel launch");
+    return SP_OK;
+}
+
+int row_copy_dt(int dtype, const void* src, void* dst, void* dst2, const sp::RowCopy& c, cudaStream_t s) {
+    return dtype == SP_F64 ? row_copy<double>(src, dst, dst2, c, s) : row_copy<float>(src, dst, dst2, c, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int sp_copy_in(const void* host, int dtype, const sp_layout* L, void* base_a, void* base_b,
+               void* staging, int64_t staging_elems, void* stream) {
+    int rc = check_layout(L, dtype);
+    if (rc) return rc;
+    if (!host || !base_a) return fail(SP_ERR_ARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t es = (size_t)elem_size(dtype);
+    const int64_t wx = L->nx + 2 * L->gx, wy = L->ny + 2 * L->gy, wz = L->nz + 2 * L->gz;
+    const int64_t corner = L->origin - L->gz * L->pz - L->gy * L->py - L->gx;
+    char* ca = (char*)base_a + corner * es;
+    char* cb = base_b ? (char*)base_b + corner * es : nullptr;
+    if (!staging) {
+        cudaMemcpy3DParms p = {};
+        p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(host), wx * es, wx, wy);
+        p.dstPtr = make_cudaPitchedPtr(ca, (size_t)L->py * es, wx, wy);
+        p.extent = make_cudaExtent(wx * es, wy, wz);
+        p.kind = cudaMemcpyDefault;
+        SP_CUDA(cudaMemcpy3DAsync(&p, s));
+        if (cb) {
+            p.srcPtr = make_cudaPitchedPtr(ca, (size_t)L->py * es, wx, wy);
+            p.dstPtr = make_cudaPitchedPtr(cb, (size_t)L->py * es, wx, wy);
+            SP_CUDA(cudaMemcpy3DAsync(&p, s));
+        }
+        return SP_OK;
+    }
+    const int64_t plane = wx * wy;
+    const int64_t chunk = staging_elems / plane;
+    if (chunk < 1) return fail(SP_ERR_ARG, "staging buffer smaller than one plane (%lld elements)",
+                               (long long)plane);
+    for (int64_t z0 = 0; z0 < wz; z0 += chunk) {
+        const int64_t n = std::min(chunk, wz - z0);
+        SP_CUDA(cudaMemcpyAsync(staging, (const char*)host + z0 * plane * es, (size_t)(n * plane) * es,
+                                cudaMemcpyDefault, s));
+        sp::RowCopy c{n, wy, wx, wx, plane, L->py, L->pz};
+        rc = row_copy_dt(dtype, staging, ca + z0 * L->pz * es, cb ? cb + z0 * L->pz * es : nullptr, c, s);
+        if (rc) return rc;
+    }
+    return SP_OK;
+}
+
+int sp_copy_out(const void* base, int dtype, const sp_layout* L, void* host, void* staging,
+                int64_t staging_elems, void* stream) {
+    int rc = check_layout(L, dtype);
+    if (rc) return rc;
+    if (!host || !base) return fail(SP_ERR_ARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t es = (size_t)elem_size(dtype);
+    const int64_t nx = L->nx, ny = L->ny, nz = L->nz;
+    const char* first = (const char*)base + L->origin * es;
+    if (!staging) {
+        cudaMemcpy3DParms p = {};
+        p.srcPtr = make_cudaPitchedPtr(const_cast<char*>(first), (size_t)L->py * es, nx,
+                                       (size_t)(L->ny + 2 * L->gy));
+        p.dstPtr = make_cudaPitchedPtr(host, nx * es, nx, ny);
+        p.extent = make_cudaExtent(nx * es, ny, nz);
+        p.kind = cudaMemcpyDefault;
+        SP_CUDA(cudaMemcpy3DAsync(&p, s));
+        return SP_OK;
+    }
+    const int64_t plane = nx * ny;
+    const int64_t chunk = staging_elems / plane;
+    if (chunk < 1) return fail(SP_ERR_ARG, "staging buffer smaller than one plane (%lld elements)",
+                               (long long)plane);
+    for (int64_t z0 = 0; z0 < nz; z0 += chunk) {
+        const int64_t n = std::min(chunk, nz - z0);
+        sp::RowCopy c{n, ny, nx, L->py, L->pz, nx, plane};
+        rc = row_copy_dt(dtype, first + z0 * L->pz * es, staging, nullptr, c, s);
+        if (rc) return rc;
+        SP_CUDA(cudaMemcpyAsync((char*)host + z0 * plane * es, staging, (size_t)(n * plane) * es,
+                                cudaMemcpyDefault, s));
+    }
+    return SP_OK;
+}
+
 int sp_ipc_export(const void* ptr, unsigned char handle[64], int64_t* offset) {
     if (!ptr || !handle || !offset) return fail(SP_ERR_ARG, "null argument");
     static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");

@@ -242,6 +242,63 @@ class TwoGrid:
     def interior(self) -> np.ndarray:
         return self.interior_device().cpu().numpy()
 
+    # -- host transfers (one pitched DMA each, stream-ordered) --------------------
+
+    def host_shape(self):
+        """Shape of the dense ghosted host field upload() takes (R/grid.py:126-134)."""
+        d = self.dims
+        return (d.nz + 2 * self.gz, d.ny + 2 * self.gxy, d.nx + 2 * self.gxy)
+
+    def upload(self, field, stream=None) -> None:
+        """Replace both arrays with a host field of shape host_shape() (torch CPU
+        tensor -- pinned for an asynchronous copy -- or numpy), as constructing
+        a reference TwoGrid from that field would; active becomes 0."""
+        import torch
+        t = field if isinstance(field, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(field))
+        if tuple(t.shape) != self.host_shape() or t.dtype != self.torch_dtype or not t.is_contiguous():
+            raise GridError(f"upload needs a contiguous {self.torch_dtype} field of shape "
+                            f"{self.host_shape()}, got {t.dtype} {tuple(t.shape)}")
+        s = self.stream() if stream is None else ctypes.c_void_p(stream)
+        self.active = 0
+        stg, n_stg = self._staging()
+        with _on(self.device):
+            N.check(N.lib().sp_copy_in(ctypes.c_void_p(t.data_ptr()), self.sp_dtype,
+                                       ctypes.byref(self.layout), ctypes.c_void_p(self._a.data_ptr()),
+                                       ctypes.c_void_p(self._b.data_ptr()), stg, n_stg, s))
+
+    STAGING_PLANES = 64
+
+    def _staging(self):
+        """Device staging buffer for host transfers: STAGING_PLANES ghosted planes
+        (linear PCIe copies, repacked on the device), allocated on first use."""
+        import torch
+        if getattr(self, "_stg", None) is None:
+            hz, hy, hx = self.host_shape()
+            n = min(hz, self.STAGING_PLANES) * hy * hx
+            with torch.cuda.device(self.device):
+                self._stg = torch.empty(n, dtype=self.torch_dtype, device=self.device)
+        return ctypes.c_void_p(self._stg.data_ptr()), self._stg.numel()
+
+    def download(self, out=None, stream=None):
+        """The current interior into host memory (a torch CPU tensor; pass a
+        pinned ``out`` of dims.shape for an asynchronous copy)."""
+        import torch
+        d = self.dims
+        fresh = out is None
+        if fresh:
+            out = torch.empty(d.shape, dtype=self.torch_dtype, pin_memory=True)
+        if tuple(out.shape) != tuple(d.shape) or out.dtype != self.torch_dtype or not out.is_contiguous():
+            raise GridError(f"download needs a contiguous {self.torch_dtype} tensor of shape {d.shape}")
+        s = self.stream() if stream is None else ctypes.c_void_p(stream)
+        with _on(self.device):
+            stg, n_stg = self._staging()
+            N.check(N.lib().sp_copy_out(ctypes.c_void_p(self.current_buffer().data_ptr()), self.sp_dtype,
+                                        ctypes.byref(self.layout), ctypes.c_void_p(out.data_ptr()),
+                                        stg, n_stg, s))
+        if fresh:
+            torch.cuda.synchronize(self.device)   # a tensor the caller did not provide: complete
+        return out
+
     def full_view(self) -> np.ndarray:
         return self.current.cpu().numpy()
 

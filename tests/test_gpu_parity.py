@@ -400,3 +400,28 @@ def test_dynamic_counter_rearms(sp, O):
     sp.sweeps(g, levels, depth=2)
     ref = oracle_run(O, shape, "random", 9, faces, levels)
     assert bitwise(g.interior(), ref.interior())
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_upload_download_round_trip(sp, O, dtype):
+    """TwoGrid.upload / download (one pitched DMA each) against the oracle."""
+    import torch
+    shape = (19, 23, 37)
+    faces = (0.3, -1.0, 2.0, 0.0, 1.0, -0.5)
+    src = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, faces, seed=4),
+                     dtype=dtype)
+    field = src.full_view()                                  # dense ghosted host field
+    g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.constant(7.0), dtype=dtype)
+    pinned = torch.from_numpy(field.copy()).pin_memory()
+    g.upload(pinned)
+    assert bitwise(g.full_view(), field)
+    assert bitwise(g.other.cpu().numpy(), field)              # B = copy of A
+    sp.sweeps(g, 6, depth=3)
+    out = torch.empty(shape, dtype=g.torch_dtype).pin_memory()
+    g.download(out)
+    torch.cuda.synchronize()
+    ref = oracle_run(O, shape, "random", 4, faces, 6, dtype=dtype)
+    assert bitwise(out.numpy(), ref.interior())
+    assert bitwise(g.download().numpy(), ref.interior())     # fresh pinned tensor, synchronised
+    with pytest.raises(sp.GridError):
+        g.upload(np.zeros((3, 3, 3), dtype=dtype))
