@@ -130,9 +130,11 @@ int sp_sweep_tb_part_peer(const void* src, void* dst, int dtype, const sp_layout
  * allocation at base_a and, if base_b is given, also base_b (B = copy of A,
  * R/grid.py:132-133).  sp_copy_out: the interior (nz, ny, nx) of the
  * allocation at base into dense host memory (TwoGrid.interior,
- * R/grid.py:151-153).  With a device staging buffer (>= one plane) the data
- * crosses PCIe as linear copies of whole planes, repacked on the device
- * (K6); without one, as a single pitched 3-D DMA. */
+ * R/grid.py:151-153).  With a device staging buffer (>= two planes) the
+ * data crosses PCIe as linear copies of whole planes through its two halves,
+ * repacked on the device (K6) on a library side stream and joined back to
+ * `stream`; without one, as a single pitched 3-D DMA.  A staging buffer must
+ * not be shared by transfers in flight at the same time. */
 int sp_copy_in(const void* host, int dtype, const sp_layout* L, void* base_a, void* base_b,
                void* staging, int64_t staging_elems, void* stream);
 int sp_copy_out(const void* base, int dtype, const sp_layout* L, void* host, void* staging,

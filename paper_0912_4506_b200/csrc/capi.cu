@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #ifndef SP_L2_PROMO
 #define SP_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
@@ -397,6 +398,73 @@ int row_copy_dt(int dtype, const void* src, void* dst, void* dst2, const sp::Row
     return dtype == SP_F64 ? row_copy<double>(src, dst, dst2, c, s) : row_copy<float>(src, dst, dst2, c, s);
 }
 
+// Side stream (one per caller stream and device) for the K6 repacks of
+// staged transfers: the PCIe copies stay on the caller's stream and run
+// ahead into the other half of the staging buffer while a repack waits for
+// SMs (a resident K2 pass holds them).  Per caller stream, so an upload and a
+// download in flight on different streams never queue behind each other.
+int side_stream(cudaStream_t caller, cudaStream_t* out) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, cudaStream_t>, cudaStream_t>> table;
+    int dev = 0;
+    SP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : table)
+        if (e.first.first == dev && e.first.second == caller) {
+            *out = e.second;
+            return SP_OK;
+        }
+    cudaStream_t r;
+    SP_CUDA(cudaStreamCreateWithFlags(&r, cudaStreamNonBlocking));
+    table.push_back({{dev, caller}, r});
+    *out = r;
+    return SP_OK;
+}
+
+// Events of one staged transfer, destroyed when it has been enqueued (CUDA
+// releases an event's resources once its pending work completes).
+struct EventSet {
+    std::vector<cudaEvent_t> ev;
+    ~EventSet() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+    int make(cudaEvent_t* e) {
+        SP_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        ev.push_back(*e);
+        return SP_OK;
+    }
+};
+
+// Staged transfer of `chunks` plane chunks through two halves of the staging
+// buffer.  upload: copy(i) on s -> repack(i) on r; download: repack(i) on r ->
+// copy(i) on s.  Buffer half i%2 is reused by chunk i+2 only after the stage
+// that reads it (repack(i) / copy(i)) has completed.
+template <typename CopyFn, typename RepackFn>
+int staged(bool upload, int64_t chunks, cudaStream_t s, CopyFn copy, RepackFn repack) {
+    cudaStream_t r;
+    int rc = side_stream(s, &r);
+    if (rc) return rc;
+    EventSet es;
+    cudaEvent_t start;
+    if ((rc = es.make(&start))) return rc;
+    SP_CUDA(cudaEventRecord(start, s));
+    SP_CUDA(cudaStreamWaitEvent(r, start, 0));
+    std::vector<cudaEvent_t> first(chunks), second(chunks);   // completion of each chunk's stages
+    for (int64_t i = 0; i < chunks; ++i) {
+        cudaStream_t s1 = upload ? s : r, s2 = upload ? r : s;
+        if (i >= 2) SP_CUDA(cudaStreamWaitEvent(s1, second[i - 2], 0));   // half i%2 is free
+        if ((rc = upload ? copy(i, s1) : repack(i, s1))) return rc;
+        if ((rc = es.make(&first[i]))) return rc;
+        SP_CUDA(cudaEventRecord(first[i], s1));
+        SP_CUDA(cudaStreamWaitEvent(s2, first[i], 0));
+        if ((rc = upload ? repack(i, s2) : copy(i, s2))) return rc;
+        if ((rc = es.make(&second[i]))) return rc;
+        SP_CUDA(cudaEventRecord(second[i], s2));
+    }
+    if (upload && chunks > 0) SP_CUDA(cudaStreamWaitEvent(s, second[chunks - 1], 0));   // join
+    return SP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -427,18 +495,23 @@ int sp_copy_in(const void* host, int dtype, const sp_layout* L, void* base_a, vo
         return SP_OK;
     }
     const int64_t plane = wx * wy;
-    const int64_t chunk = staging_elems / plane;
-    if (chunk < 1) return fail(SP_ERR_ARG, "staging buffer smaller than one plane (%lld elements)",
-                               (long long)plane);
-    for (int64_t z0 = 0; z0 < wz; z0 += chunk) {
-        const int64_t n = std::min(chunk, wz - z0);
-        SP_CUDA(cudaMemcpyAsync(staging, (const char*)host + z0 * plane * es, (size_t)(n * plane) * es,
-                                cudaMemcpyDefault, s));
+    const int64_t chunk = staging_elems / (2 * plane);   // two halves
+    if (chunk < 1) return fail(SP_ERR_ARG, "staging buffer smaller than two planes (%lld elements)",
+                               (long long)(2 * plane));
+    const int64_t chunks = (wz + chunk - 1) / chunk;
+    auto half = [&](int64_t i) { return (char*)staging + (i & 1) * chunk * plane * es; };
+    auto copy = [&](int64_t i, cudaStream_t st) -> int {
+        const int64_t z0 = i * chunk, n = std::min(chunk, wz - z0);
+        SP_CUDA(cudaMemcpyAsync(half(i), (const char*)host + z0 * plane * es, (size_t)(n * plane) * es,
+                                cudaMemcpyDefault, st));
+        return SP_OK;
+    };
+    auto repack = [&](int64_t i, cudaStream_t st) -> int {
+        const int64_t z0 = i * chunk, n = std::min(chunk, wz - z0);
         sp::RowCopy c{n, wy, wx, wx, plane, L->py, L->pz};
-        rc = row_copy_dt(dtype, staging, ca + z0 * L->pz * es, cb ? cb + z0 * L->pz * es : nullptr, c, s);
-        if (rc) return rc;
-    }
-    return SP_OK;
+        return row_copy_dt(dtype, half(i), ca + z0 * L->pz * es, cb ? cb + z0 * L->pz * es : nullptr, c, st);
+    };
+    return staged(true, chunks, s, copy, repack);
 }
 
 int sp_copy_out(const void* base, int dtype, const sp_layout* L, void* host, void* staging,
@@ -461,18 +534,23 @@ int sp_copy_out(const void* base, int dtype, const sp_layout* L, void* host, voi
         return SP_OK;
     }
     const int64_t plane = nx * ny;
-    const int64_t chunk = staging_elems / plane;
-    if (chunk < 1) return fail(SP_ERR_ARG, "staging buffer smaller than one plane (%lld elements)",
-                               (long long)plane);
-    for (int64_t z0 = 0; z0 < nz; z0 += chunk) {
-        const int64_t n = std::min(chunk, nz - z0);
+    const int64_t chunk = staging_elems / (2 * plane);   // two halves
+    if (chunk < 1) return fail(SP_ERR_ARG, "staging buffer smaller than two planes (%lld elements)",
+                               (long long)(2 * plane));
+    const int64_t chunks = (nz + chunk - 1) / chunk;
+    auto half = [&](int64_t i) { return (char*)staging + (i & 1) * chunk * plane * es; };
+    auto repack = [&](int64_t i, cudaStream_t st) -> int {
+        const int64_t z0 = i * chunk, n = std::min(chunk, nz - z0);
         sp::RowCopy c{n, ny, nx, L->py, L->pz, nx, plane};
-        rc = row_copy_dt(dtype, first + z0 * L->pz * es, staging, nullptr, c, s);
-        if (rc) return rc;
-        SP_CUDA(cudaMemcpyAsync((char*)host + z0 * plane * es, staging, (size_t)(n * plane) * es,
-                                cudaMemcpyDefault, s));
-    }
-    return SP_OK;
+        return row_copy_dt(dtype, first + z0 * L->pz * es, half(i), nullptr, c, st);
+    };
+    auto copy = [&](int64_t i, cudaStream_t st) -> int {
+        const int64_t z0 = i * chunk, n = std::min(chunk, nz - z0);
+        SP_CUDA(cudaMemcpyAsync((char*)host + z0 * plane * es, half(i), (size_t)(n * plane) * es,
+                                cudaMemcpyDefault, st));
+        return SP_OK;
+    };
+    return staged(false, chunks, s, copy, repack);
 }
 
 int sp_ipc_export(const void* ptr, unsigned char handle[64], int64_t* offset) {
