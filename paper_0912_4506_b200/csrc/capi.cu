@@ -131,6 +131,7 @@ struct Variant {
     int by, py, slots, minb, ring;   // warps, rows/thread, z-queue slots, CTAs/SM, TMA ring cap
     int rstore;                      // 1: running output pointer (see tb_kernel)
     int split;                       // 1: split step barrier (see tb_kernel)
+    int zcap = 0;                    // > 0: z-chunks at most this many planes (L2 locality)
 };
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
@@ -141,8 +142,8 @@ constexpr Variant kVariants[] = {
     {16, 2, 3, 1, 6, 0, 0},  // 5: fp64 T=1 (shallower ring streams better)
     {16, 2, 1, 1, 8, 0, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
     {8, 4, 1, 1, 8, 0, 0},   // 7: same, 8 warps
-    {8, 8, 2, 1, 8, 1, 0},   // 8: fp32 T=3,4: 4 with the running output pointer
-    {8, 4, 2, 2, 8, 0, 1},   // 9: fp64 T=2: two CTAs per SM (<= 128 registers), split
+    {8, 8, 2, 1, 8, 1, 0, 128},  // 8: fp32 T=3,4: 4 with the running output pointer
+    {8, 4, 2, 2, 8, 0, 1, 80},   // 9: fp64 T=2: two CTAs per SM (<= 128 registers), split
     {8, 4, 1, 2, 8, 0, 0},   // 10: two CTAs per SM, z-queue v[p-1] from shared memory
     {16, 2, 2, 1, 8, 0, 1},  // 11: fp32 T=5,6: 0 with the split barrier
     {8, 4, 2, 1, 8, 0, 1},   // 12: fp64 T>4: 2 with the split barrier
@@ -730,10 +731,15 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     const int slots = di.sms * kVariants[variant].minb;
     // z-chunking: minimise waves * (chunk + 2T) -- the wave-quantised cost of
     // every unit streaming chunk+2T planes.
+    // Short chunks keep the units in flight close in z, so neighbouring
+    // tiles' shared halo rows are still in L2 when the second one reads them
+    // (dynamic schedule): variants tuned for it cap the chunk length.
     int64_t best_n = 1;
     double best_cost = 1e300;
     const int64_t max_chunks = std::min<int64_t>(nzb, 256);
-    for (int64_t nch = 1; nch <= max_chunks; ++nch) {
+    const int zcap = g_dynamic ? kVariants[variant].zcap : 0;
+    const int64_t min_chunks = zcap > 0 ? std::min<int64_t>(max_chunks, (nzb + zcap - 1) / zcap) : 1;
+    for (int64_t nch = min_chunks; nch <= max_chunks; ++nch) {
         int64_t len = (nzb + nch - 1) / nch;
         int64_t nreal = (nzb + len - 1) / len;
         int64_t units = tiles * nreal;
