@@ -138,7 +138,7 @@ constexpr Variant kVariants[] = {
     {16, 2, 3, 1, 8, 0, 1},  // 1: fp64 T=3
     {8, 4, 2, 1, 8, 0, 0},   // 2: fp32 T>6
     {8, 4, 3, 1, 8, 0, 1},   // 3
-    {8, 8, 2, 1, 8, 0, 0},   // 4: fp32 T=2 (64x64 footprint)
+    {8, 8, 2, 1, 8, 0, 0},   // 4: 64x64 footprint
     {16, 2, 3, 1, 6, 0, 0},  // 5: fp64 T=1 (shallower ring streams better)
     {16, 2, 1, 1, 8, 0, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
     {8, 4, 1, 1, 8, 0, 0},   // 7: same, 8 warps
@@ -150,8 +150,9 @@ constexpr Variant kVariants[] = {
     {8, 4, 3, 1, 8, 0, 0},   // 13: 3 with __syncthreads
     {16, 2, 3, 1, 8, 0, 0},  // 14: fp32 T=1: 1 with __syncthreads
     {8, 4, 3, 1, 8, 1, 1},   // 15: fp64 T=4: 3 with the running output pointer
+    {8, 8, 2, 2, 8, 1, 1, 128},  // 16: fp32 T=2: 8 at two CTAs per SM, split
 };
-constexpr int kNumVariants = 16;
+constexpr int kNumVariants = 17;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
@@ -163,6 +164,7 @@ constexpr bool compiled() {
     if (T == 1) return V == 5 || V == 14;
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
+    if (V == 16) return sizeof(R) == 4 && T == 2;   // deeper: spills at 128 registers
     if (V == 11) return true;
     if (V == 4) return T <= 4;
     if (V == 2 || V == 12) return T >= 3;
@@ -183,7 +185,7 @@ int default_variant(int dtype, int T) {
     }
     switch (T) {
         case 1: return 14;       // 16x2/3
-        case 2: return 4;        // 8x8/2 (64x64 footprint)
+        case 2: return 16;       // 8x8/2, two CTAs per SM, split
         case 3:
         case 4: return 8;        // 8x8/2, running output pointer
         case 5:
@@ -216,7 +218,8 @@ bool is_usable(int v) {
         case 12: return usable<R, T, 12>();
         case 13: return usable<R, T, 13>();
         case 14: return usable<R, T, 14>();
-        default: return usable<R, T, 15>();
+        case 15: return usable<R, T, 15>();
+        default: return usable<R, T, 16>();
     }
 }
 
@@ -300,7 +303,8 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 12: return launch_tb_t<R, T, 12>(src, L, a, grid, s);
         case 13: return launch_tb_t<R, T, 13>(src, L, a, grid, s);
         case 14: return launch_tb_t<R, T, 14>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 15>(src, L, a, grid, s);
+        case 15: return launch_tb_t<R, T, 15>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 16>(src, L, a, grid, s);
     }
 }
 
