@@ -140,11 +140,11 @@ constexpr Variant kVariants[] = {
     {8, 4, 3, 1, 8, 0, 1},   // 3
     {8, 8, 2, 1, 8, 0, 0},   // 4: 64x64 footprint
     {16, 2, 3, 1, 6, 0, 0},  // 5: fp64 T=1 (shallower ring streams better)
-    {16, 2, 1, 1, 8, 0, 0},  // 6: v[p-1] re-read from shared memory (16 warps)
-    {8, 4, 1, 1, 8, 0, 0},   // 7: same, 8 warps
+    {16, 2, 1, 1, 8, 0, 1},  // 6: v[p-1] re-read from shared memory (16 warps), split
+    {8, 4, 1, 1, 8, 0, 1},   // 7: same, 8 warps
     {8, 8, 2, 1, 8, 1, 0, 128},  // 8: fp32 T=3,4: 4 with the running output pointer
     {8, 4, 2, 2, 8, 0, 1, 80},   // 9: fp64 T=2: two CTAs per SM (<= 128 registers), split
-    {8, 4, 1, 2, 8, 0, 0},   // 10: two CTAs per SM, z-queue v[p-1] from shared memory
+    {8, 4, 1, 2, 8, 0, 1, 80},   // 10: two CTAs per SM, z-queue v[p-1] from shared memory, split
     {16, 2, 2, 1, 8, 0, 1},  // 11: fp32 T=5,6: 0 with the split barrier
     {8, 4, 2, 1, 8, 0, 1},   // 12: fp64 T>4: 2 with the split barrier
     {8, 4, 3, 1, 8, 0, 0},   // 13: 3 with __syncthreads

@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     // (the level-1 edge-row store).  The TMA wait, ring loads and level-1
     // arithmetic of step k overlap the slowest warps of step k-1; thread 0
     // refills the ring slot freed by step k-1 right after that wait.
-    constexpr bool SPLIT = SPLITV && T >= 2 && P::DB && SLOTS != 1;
+    constexpr bool SPLIT = SPLITV && T >= 2 && P::DB;
 
     const int lane = threadIdx.x & 31;
     const int wy = threadIdx.x >> 5;
@@ -455,7 +455,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     mbar_wait(&lbar[k1 & 1u], (k1 >> 1) & 1u);
                     if (threadIdx.x == 0) {
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        produce(pslot2);   // ring slot of plane k-2, last read in step k-1
+                        // ring slot last read in step k-1: plane k-2 (k-3 with SLOTS == 1,
+                        // which re-reads v[p-1] from slot k-2 at the start of a step)
+                        produce(SLOTS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
                     }
                 }
                 if (t < T) {
