@@ -13,6 +13,7 @@
 #include <cstring>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -132,6 +133,7 @@ struct Variant {
     int rstore;                      // 1: running output pointer (see tb_kernel)
     int split;                       // 1: split step barrier (see tb_kernel)
     int zcap = 0;                    // > 0: z-chunks at most this many planes (L2 locality)
+    int cl = 1;                      // > 1: y-cooperative thread-block clusters of this size
 };
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
@@ -151,8 +153,12 @@ constexpr Variant kVariants[] = {
     {16, 2, 3, 1, 8, 0, 0},  // 14: fp32 T=1: 1 with __syncthreads
     {8, 4, 3, 1, 8, 1, 1},   // 15: fp64 T=4: 3 with the running output pointer
     {8, 8, 2, 2, 8, 1, 1, 128},  // 16: fp32 T=2: 8 at two CTAs per SM, split
+    // y-cooperative clusters (footprint 64 x cl*WY, edge rows over DSMEM)
+    {8, 4, 2, 2, 8, 0, 1, 0, 4},   // 17: 9 in clusters of 4
+    {16, 2, 3, 1, 8, 0, 1, 0, 4},  // 18: 1 in clusters of 4
+    {8, 4, 2, 2, 8, 1, 1, 80},     // 19: 9 with the running output pointer
 };
-constexpr int kNumVariants = 17;
+constexpr int kNumVariants = 20;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
@@ -162,6 +168,9 @@ template <typename R, int T, int V>
 constexpr bool compiled() {
     if (V == 0) return true;
     if (T == 1) return V == 5 || V == 14;
+    if (V == 17 || V == 18) return sizeof(R) == 8 && T >= 2 && T <= 4;
+    if (V == 19) return T == 2;
+
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
     if (V == 16) return sizeof(R) == 4 && T == 2;   // deeper: spills at 128 registers
@@ -197,7 +206,7 @@ int default_variant(int dtype, int T) {
 template <typename R, int T, int V>
 constexpr bool usable() {
     constexpr Variant v = kVariants[V];
-    return compiled<R, T, V>() && sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>::FITS;
+    return compiled<R, T, V>() && sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.cl>::FITS;
 }
 
 template <typename R, int T>
@@ -219,7 +228,10 @@ bool is_usable(int v) {
         case 13: return usable<R, T, 13>();
         case 14: return usable<R, T, 14>();
         case 15: return usable<R, T, 15>();
-        default: return usable<R, T, 16>();
+        case 16: return usable<R, T, 16>();
+        case 17: return usable<R, T, 17>();
+        case 18: return usable<R, T, 18>();
+        default: return usable<R, T, 19>();
     }
 }
 
@@ -251,8 +263,8 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
     } else {
         constexpr Variant v = kVariants[V];
-        using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER>;
+        using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.cl>;
+        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER, v.cl>;
         const size_t smem = Pl::SMEM;
         // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
         static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
@@ -269,14 +281,46 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         cuuint64_t gdim[3] = {(cuuint64_t)L->py, (cuuint64_t)(L->ny + 2 * L->gy),
                               (cuuint64_t)(L->nz + 2 * L->gz)};
         cuuint64_t gstride[2] = {(cuuint64_t)(L->py * sizeof(R)), (cuuint64_t)(L->pz * sizeof(R))};
-        cuuint32_t box[3] = {(cuuint32_t)sp::WX, (cuuint32_t)Pl::WY, 1};
+        cuuint32_t box[3] = {(cuuint32_t)sp::WX, (cuuint32_t)Pl::RROWS, 1};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = enc(&map, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                          3, const_cast<void*>(src), gdim, gstride, box, estr,
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          SP_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-        kern<<<grid, Pl::NT, smem, stream>>>(map, a);
+        if constexpr (v.cl > 1) {
+            // persistent clusters: as many as can be co-resident, round-robin units
+            static std::atomic<uint64_t> occ[64] = {};   // per device: active clusters + 1
+            cudaLaunchConfig_t cfg = {};
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = v.cl;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.blockDim = dim3(Pl::NT, 1, 1);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = stream;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            uint64_t nc = occ[dev & 63].load();
+            if (nc == 0) {
+                if (v.cl > 8) SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                int n = 0;
+                cfg.gridDim = dim3(v.cl * 148, 1, 1);
+                SP_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+                if (n < 1) return fail(SP_ERR_DEVICE, "no cluster of %d CTAs fits (variant %d)", v.cl, V);
+                nc = (uint64_t)n + 1;
+                occ[dev & 63].store(nc);
+                if (getenv("SP_DEBUG_CLUSTER"))
+                    fprintf(stderr, "[sp] variant %d T=%d: %d active clusters of %d CTAs (smem %zu)\n", V, T, n,
+                            v.cl, smem);
+            }
+            const int clusters = (int)std::min<int64_t>(a.units, (int64_t)(nc - 1));
+            cfg.gridDim = dim3(clusters * v.cl, 1, 1);
+            SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a));
+        } else {
+            kern<<<grid, Pl::NT, smem, stream>>>(map, a);
+        }
         g_launches.fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "tb_kernel launch");
@@ -304,7 +348,10 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 13: return launch_tb_t<R, T, 13>(src, L, a, grid, s);
         case 14: return launch_tb_t<R, T, 14>(src, L, a, grid, s);
         case 15: return launch_tb_t<R, T, 15>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 16>(src, L, a, grid, s);
+        case 16: return launch_tb_t<R, T, 16>(src, L, a, grid, s);
+        case 17: return launch_tb_t<R, T, 17>(src, L, a, grid, s);
+        case 18: return launch_tb_t<R, T, 18>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 19>(src, L, a, grid, s);
     }
 }
 
@@ -723,7 +770,8 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     else
         a.ox = sp::WX - 2 * T - (A - 1);
     const int variant = peer ? kPeerVariant : variant_for(dtype, T);
-    const int wy = kVariants[variant].by * kVariants[variant].py;
+    const int cl = kVariants[variant].cl;
+    const int wy = kVariants[variant].by * kVariants[variant].py * cl;   // cluster footprint rows
     if (wy - 2 * T < 1) return fail(SP_ERR_SCHEDULE, "depth T=%d too deep for a %d-row footprint", T, wy);
     a.oy = wy - 2 * T;
     a.ntx = (int)((out_hi[2] - out_lo[2] + a.ox - 1) / a.ox);
@@ -732,7 +780,7 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     a.gz = (int)L->gz;
     const int64_t nzb = out_hi[0] - out_lo[0];
     const int64_t tiles = (int64_t)a.ntx * a.nty;
-    const int slots = di.sms * kVariants[variant].minb;
+    const int slots = std::max(1, di.sms * kVariants[variant].minb / cl);   // concurrent units
     // z-chunking: minimise waves * (chunk + 2T) -- the wave-quantised cost of
     // every unit streaming chunk+2T planes.
     // Short chunks keep the units in flight close in z, so neighbouring
@@ -759,7 +807,7 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     a.units = (int)(tiles * nch);
     a.strip = g_strip;
     a.sched = nullptr;
-    if (g_dynamic) {
+    if (g_dynamic && cl == 1) {
         rc = sched_counter(&a.sched);
         if (rc) return rc;
     }

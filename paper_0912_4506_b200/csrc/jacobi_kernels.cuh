@@ -90,6 +90,92 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// ---- thread-block clusters (y-cooperative K2) ----------------------------------
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_id_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_count_x() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// shared::cluster address of `p` (own shared memory) in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+
+// release at cluster scope: this warp's level-plane stores (made visible to
+// lane 0 by __syncwarp) happen before the neighbour's acquire
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+
+// wait with cluster-scope acquire: writes a neighbour CTA made before its
+// (remote, release.cluster) arrive are visible afterwards
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    uint32_t addr = smem_u32(bar);
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+template <typename R> struct SmemLd;
+template <> struct SmemLd<double> {
+    __device__ static __forceinline__ double2 v2(const void* p) {
+        double2 r;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(smem_u32(p)) : "memory");
+        return r;
+    }
+};
+template <> struct SmemLd<float> {
+    __device__ static __forceinline__ float2 v2(const void* p) {
+        float2 r;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(smem_u32(p)) : "memory");
+        return r;
+    }
+};
+
+template <typename R> struct DsmemLd;
+template <> struct DsmemLd<double> {
+    __device__ static __forceinline__ double2 v2(uint32_t addr) {
+        double2 r;
+        asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(addr) : "memory");
+        return r;
+    }
+};
+template <> struct DsmemLd<float> {
+    __device__ static __forceinline__ float2 v2(uint32_t addr) {
+        float2 r;
+        asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(r.x), "=f"(r.y) : "r"(addr) : "memory");
+        return r;
+    }
+};
+
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2) {
     asm volatile(
@@ -159,7 +245,7 @@ __device__ __forceinline__ int footprint_x(const TBArgs& a, int x0, int T) {
 // Shared-memory plan per instantiation: a RING-deep TMA ring of level-0
 // planes plus, for levels 1..T-1, one plane each -- double-buffered when it
 // fits (one barrier per step), single-buffered otherwise (two barriers).
-template <typename R, int T, int BY, int PY, int SLOTS = 3, int MINB = 1, int RCAP = 8>
+template <typename R, int T, int BY, int PY, int SLOTS = 3, int MINB = 1, int RCAP = 8, int CL = 1>
 struct Plan {
     // SLOTS == 1 keeps only v[p] in registers; v[p-1] is re-read from the
     // double-buffered level plane (and ring slot k-2) just before it is
@@ -169,35 +255,55 @@ struct Plan {
     static constexpr int NT = 32 * BY;
     static constexpr int PLANE = WX * WY;
     static constexpr int PLANE_BYTES = PLANE * (int)sizeof(R);
+    // Clusters (CL > 1): the ring's level-0 planes carry HR extra rows above
+    // and below the CTA's rows (level 1's y-neighbours at the CTA edges);
+    // deeper levels take them from the neighbour CTAs' level planes (DSMEM).
+    static constexpr int HR = CL > 1 ? 1 : 0;
+    static constexpr int RROWS = WY + 2 * HR;
+    static constexpr int RPLANE = WX * RROWS;
+    static constexpr int RPLANE_BYTES = RPLANE * (int)sizeof(R);
     // opt-in smem per CTA (MINB CTAs share the SM's 228 KB), minus barriers
     static constexpr int BUDGET = (MINB == 1 ? 232448 : 233472 / MINB - 1024) - 256;
     static constexpr int NL = (T > 1) ? (T - 1) : 0;        // stored level planes
-    static constexpr bool DB = (2 * NL + 3) * PLANE_BYTES <= BUDGET;
+    static constexpr bool DB = 2 * NL * PLANE_BYTES + 3 * RPLANE_BYTES <= BUDGET;
     static constexpr int NBUF = DB ? 2 : 1;
-    static constexpr int RING_FIT = BUDGET / PLANE_BYTES - NBUF * NL;
+    static constexpr int RING_FIT = (BUDGET - NBUF * NL * PLANE_BYTES) / RPLANE_BYTES;
     static constexpr int RING = RING_FIT > RCAP ? RCAP : RING_FIT;
     static constexpr int MIN_RING = SLOTS == 1 ? 4 : 3;
-    static constexpr bool FITS = RING >= MIN_RING && WY - 2 * T >= 1 && (SLOTS != 1 || DB);
+    static constexpr bool FITS = RING >= MIN_RING && CL * WY - 2 * T >= 1 && (SLOTS != 1 || DB) &&
+                                 (CL == 1 || (DB && SLOTS != 1 && T >= 2));
     static constexpr int NUID = 16;   // unit ids handed from the producer to the consumers
-    static constexpr size_t SMEM = (size_t)(RING + NBUF * NL) * PLANE_BYTES + (RING + 2) * 8 + NUID * 4;
+    static constexpr size_t SMEM =
+        (size_t)RING * RPLANE_BYTES + (size_t)NBUF * NL * PLANE_BYTES + (RING + 2) * 8 + NUID * 4;
 };
 
+// CL > 1 (y-cooperative clusters): CL CTAs of a cluster own CL vertically
+// adjacent WY-row slices of one 64 x CL*WY footprint; a slice's edge rows of
+// levels >= 2 come from the neighbour slices' level planes over DSMEM
+// instead of being recomputed, so the overlapped (redundant) halo is
+// paid once per cluster footprint, not per CTA.  The split step barrier
+// spans the cluster: each CTA's edge warps also arrive on the neighbour
+// CTA's step barrier.  Units are assigned round-robin per cluster.
 template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV,
-          bool PEER = false>
+          bool PEER = false, int CL = 1>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
     constexpr int QN = SLOTS == 1 ? 2 : SLOTS;   // register slots per level
     using A = Arith<R>;
     using V2 = typename A::V2;
-    using P = Plan<R, T, BY, PY, SLOTS, MINB, RCAP>;
+    using P = Plan<R, T, BY, PY, SLOTS, MINB, RCAP, CL>;
     constexpr int WY = P::WY;
     constexpr int PLANE = P::PLANE;
+    constexpr int RPLANE = P::RPLANE;
+    constexpr int HR = P::HR;
     constexpr int RING_N = P::RING;
+    static_assert(CL == 1 || (SPLITV && P::DB && SLOTS != 1 && T >= 2 && !PEER),
+                  "cluster variants need the split barrier, double-buffered planes, 2-3 slots");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     R* ring = reinterpret_cast<R*>(smem_raw);
-    R* lvl = ring + RING_N * PLANE;  // [level-1][buf] planes for levels 1..T-1
+    R* lvl = ring + RING_N * RPLANE;  // [level-1][buf] planes for levels 1..T-1
     uint64_t* full = reinterpret_cast<uint64_t*>(lvl + P::NBUF * P::NL * PLANE);
     uint64_t* lbar = full + RING_N;   // [2]: step-parity barriers of the level planes (SPLIT)
     volatile int* uid = reinterpret_cast<volatile int*>(lbar + 2);
@@ -215,15 +321,26 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     const int cy = wy * PY;    // footprint-local y of the thread's first row
     const int cym = max(cy - 1, 0);
     const int cyp = min(cy + PY, WY - 1);
-    constexpr uint32_t kPlaneBytes = P::PLANE_BYTES;
+    constexpr uint32_t kRingBytes = P::RPLANE_BYTES;
 
+    const int crank = CL > 1 ? (int)cluster_rank() : 0;
+    const bool has_up = CL > 1 && crank > 0, has_dn = CL > 1 && crank < CL - 1;
     if (threadIdx.x == 0) {
         for (int i = 0; i < RING_N; ++i) mbar_init(&full[i], 1);
-        mbar_init(&lbar[0], BY);
-        mbar_init(&lbar[1], BY);
+        // own warps, plus the neighbour CTAs' edge warps that read/write our edge rows
+        const uint32_t nb = BY + (has_up ? 1 : 0) + (has_dn ? 1 : 0);
+        mbar_init(&lbar[0], nb);
+        mbar_init(&lbar[1], nb);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();
+    if constexpr (CL > 1) cluster_sync_all();   // neighbours' barriers exist before any remote arrive
+    else __syncthreads();
+    // DSMEM addresses of the neighbour slices' step barriers and level planes
+    uint32_t up_lbar = 0, dn_lbar = 0, up_lvl = 0, dn_lvl = 0;
+    if constexpr (CL > 1) {
+        if (has_up) { up_lbar = map_rank(lbar, crank - 1); up_lvl = map_rank(lvl, crank - 1); }
+        if (has_dn) { dn_lbar = map_rank(lbar, crank + 1); dn_lvl = map_rank(lvl, crank + 1); }
+    }
 
     // Producer (thread 0 only): claims units -- from the device counter
     // (dynamic) or round-robin (static) -- publishes each id in uid[] ahead
@@ -235,7 +352,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     int pu = -1, pseq = 0, pc0 = 0, pc1 = 0, pc2 = 0, pc2_end = 0;
     bool pdone = false;
     auto producer_unit = [&]() {
-        if (a.sched) {
+        if constexpr (CL > 1) {
+            pu = pseq == 0 ? (int)cluster_id_x() : pu + (int)cluster_count_x();
+        } else if (a.sched) {
             pu = (int)atomicAdd(a.sched, 1u);
             // every CTA overshoots exactly once; the last overshoot re-arms the counter
             if (pu == a.units + (int)gridDim.x - 1) atomicExch(a.sched, 0u);
@@ -246,7 +365,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         if (pu >= a.units) return;
         const Unit pw = decode_unit(a, pu);
         pc0 = footprint_x<R>(a, pw.x0, T) + a.x_off;
-        pc1 = pw.y0 - T + a.gy;
+        pc1 = pw.y0 - T + crank * WY - HR + a.gy;
         pc2 = pw.zc0 - T + a.gz;
         pc2_end = pw.zc1 + T + a.gz;
     };
@@ -257,8 +376,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             pdone = true;
             return;
         }
-        mbar_expect_tx(&full[slot], kPlaneBytes);
-        tma_load_3d(ring + slot * PLANE, &tmap, &full[slot], pc0, pc1, pc2);
+        mbar_expect_tx(&full[slot], kRingBytes);
+        tma_load_3d(ring + slot * RPLANE, &tmap, &full[slot], pc0, pc1, pc2);
         if (++pc2 == pc2_end) producer_unit();
     };
     if (threadIdx.x == 0) {
@@ -276,7 +395,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         const int u = uid[cseq & (P::NUID - 1)];
         if (u < 0) break;
         const Unit w = decode_unit(a, u);
-        const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T;
+        const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T + crank * WY;
         const int nsteps = (w.zc1 - w.zc0) + 2 * T;
 
         // Per-level x/y domain of this thread's columns: x bits (PX per level)
@@ -324,6 +443,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         R* dnext = dcol + (int64_t)(w.zc0 - 2 * T) * pz;   // plane q-T of step 0
         // both x cells written and the pair 16-byte aligned (same for every row: py is)
         const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
+        // every row of the patch is written with one 16-byte store (interior tiles)
+        const bool full_rows = vec_store && wyb == (1u << PY) - 1u;
 
         // Per level t < T, a register z-queue.  SLOTS == 3: three slots
         // rotating with the step phase -- at phase f, Q[f] = v[p-1],
@@ -353,6 +474,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             constexpr int F1 = SLOTS == 3 ? (PH + 1) % 3 : (SLOTS == 1 ? PH : 1);    // v[p]
             constexpr int F2 = SLOTS == 3 ? (PH + 2) % 3 : (SLOTS == 1 ? PH ^ 1 : 0); // v[p+1]
             constexpr bool FAST = decltype(fast)::value;
+
             const int slot = gstep % RING_N;
             const int pslot = (gstep + RING_N - 1) % RING_N;
             const int pslot2 = (gstep + RING_N - 2) % RING_N;
@@ -365,10 +487,24 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             // lane-neighbour cells from the registers of Q[F1]).
             R s[T][PY][PX];
             auto xy_sums = [&](int t) {
-                const R* Pl = (t == 1) ? ring + pslot * PLANE : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
+                const R* Pl = (t == 1) ? ring + pslot * RPLANE + HR * WX
+                                       : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
                 const R(&v)[PY][PX] = Q[F1][t - 1];
-                V2 up = *reinterpret_cast<const V2*>(Pl + cym * WX + cx);
-                V2 dn = *reinterpret_cast<const V2*>(Pl + cyp * WX + cx);
+                V2 up, dn;
+                if constexpr (CL > 1) {
+                    // level 0: the ring's halo rows; deeper: the neighbour slice's
+                    // edge row of the previous step (DSMEM), own slice otherwise
+                    const uint32_t off = (uint32_t)((((t - 2) * P::NBUF + prv) * PLANE + cx) * sizeof(R));
+                    if (t == 1) up = SmemLd<R>::v2(Pl + (cy - 1) * WX + cx);
+                    else if (wy == 0 && has_up) up = DsmemLd<R>::v2(up_lvl + off + (WY - 1) * WX * sizeof(R));
+                    else up = SmemLd<R>::v2(Pl + cym * WX + cx);
+                    if (t == 1) dn = SmemLd<R>::v2(Pl + (cy + PY) * WX + cx);
+                    else if (wy == BY - 1 && has_dn) dn = DsmemLd<R>::v2(dn_lvl + off);
+                    else dn = SmemLd<R>::v2(Pl + cyp * WX + cx);
+                } else {
+                    up = *reinterpret_cast<const V2*>(Pl + cym * WX + cx);
+                    dn = *reinterpret_cast<const V2*>(Pl + cyp * WX + cx);
+                }
 #pragma unroll
                 for (int j = 0; j < PY; ++j) {
                     R lft = __shfl_up_sync(0xffffffffu, v[j][1], 1);
@@ -397,7 +533,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             // SLOTS == 1: v[p-1] of level t-1, re-read from shared memory
             R mv[SLOTS == 1 ? PY : 1][PX];
             if constexpr (SLOTS == 1) {
-                const R* L2 = ring + pslot2 * PLANE;   // level 0, plane q-2
+                const R* L2 = ring + pslot2 * RPLANE;   // level 0, plane q-2
 #pragma unroll
                 for (int j = 0; j < PY; ++j) {
                     V2 r = *reinterpret_cast<const V2*>(L2 + (cy + j) * WX + cx);
@@ -406,7 +542,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 }
             }
             {
-                const R* L0 = ring + slot * PLANE;
+                const R* L0 = ring + slot * RPLANE + HR * WX;
                 R(&n0)[PY][PX] = newv(0);
 #pragma unroll
                 for (int j = 0; j < PY; ++j) {
@@ -452,7 +588,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     // step k-1 is complete in every warp: its reads of this
                     // buffer are done and its level planes are visible
                     const uint32_t k1 = gstep - 1;
-                    mbar_wait(&lbar[k1 & 1u], (k1 >> 1) & 1u);
+                    // only the edge warps read a neighbour's planes: cluster-scope acquire
+                    if (CL > 1 && ((wy == 0 && has_up) || (wy == BY - 1 && has_dn)))
+                        mbar_wait_cluster(&lbar[k1 & 1u], (k1 >> 1) & 1u);
+                    else
+                        mbar_wait(&lbar[k1 & 1u], (k1 >> 1) & 1u);
                     if (threadIdx.x == 0) {
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         // ring slot last read in step k-1: plane k-2 (k-3 with SLOTS == 1,
@@ -490,12 +630,16 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             if (st >= 2 * T) {
                 R* d = RSTORE ? dnext : dcol + (int64_t)(q - T) * pz;
                 auto put = [&](R* b) {
-                    if (vec_store) {
+                    if (full_rows) {
+#pragma unroll
+                        for (int j = 0; j < PY; ++j)
+                            __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
+                    } else if (vec_store) {
 #pragma unroll
                         for (int j = 0; j < PY; ++j)
                             if ((wyb >> j) & 1u)
                                 __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
-                    } else {
+                    } else if (wx != 0u) {   // lanes with no output column skip the whole block
 #pragma unroll
                         for (int j = 0; j < PY; ++j) {
                             const bool row = (wyb >> j) & 1u;
@@ -514,7 +658,14 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             if (RSTORE) dnext += pz;
             if constexpr (SPLIT) {
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&lbar[gstep & 1u]);
+                if (lane == 0) {
+                    mbar_arrive(&lbar[gstep & 1u]);
+                    if constexpr (CL > 1) {
+                        // our edge rows of this step are stored / the neighbour's are read
+                        if (wy == 0 && has_up) mbar_arrive_remote(up_lbar + 8u * (gstep & 1u));
+                        if (wy == BY - 1 && has_dn) mbar_arrive_remote(dn_lbar + 8u * (gstep & 1u));
+                    }
+                }
             } else {
                 __syncthreads();
                 // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
@@ -552,6 +703,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             for (int st = 0; st < nsteps; ++st) run(std::integral_constant<int, 0>{}, st);
         }
     }
+    // no CTA leaves while a neighbour may still read its planes or arrive on its barriers
+    if constexpr (CL > 1) cluster_sync_all();
 }
 
 // ---- K1: single-level streaming sweep ---------------------------------------
