@@ -347,9 +347,9 @@ def main():
     e2e = None
     if not args.no_e2e:
         if not use_runner:
-            # a stream of independent problems: >= 10 steps so the pipeline's fill
+            # a stream of independent problems: >= 24 steps so the pipeline's fill
             # (first upload) and drain (last download) are a small share
-            e2e = measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=max(args.steps, 10))
+            e2e = measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=max(args.steps, 24))
         else:
             e2e = measure_e2e_dist(torch, dist, runner, passes, dev, world, steps=max(args.steps, 3))
 
