@@ -157,8 +157,12 @@ constexpr Variant kVariants[] = {
     {8, 4, 2, 2, 8, 0, 1, 0, 4},   // 17: 9 in clusters of 4
     {16, 2, 3, 1, 8, 0, 1, 0, 4},  // 18: 1 in clusters of 4
     {8, 4, 2, 2, 8, 1, 1, 80},     // 19: 9 with the running output pointer
+    // 12 warps x 3 rows (64x36 footprint): 3 warps per scheduler at <= 168 registers
+    {12, 3, 2, 1, 8, 1, 1},        // 20: fp64 T=4 alternative (ties 15)
+    {12, 3, 3, 1, 8, 1, 1},        // 21: fp64 T=3
+    {12, 6, 2, 1, 8, 1, 0, 128},   // 22: fp32 T=3 (64x72 footprint)
 };
-constexpr int kNumVariants = 20;
+constexpr int kNumVariants = 23;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
@@ -170,6 +174,8 @@ constexpr bool compiled() {
     if (T == 1) return V == 5 || V == 14;
     if (V == 17 || V == 18) return sizeof(R) == 8 && T >= 2 && T <= 4;
     if (V == 19) return T == 2;
+    if (V == 20 || V == 21) return sizeof(R) == 8 && T >= 3 && T <= 4;
+    if (V == 22) return sizeof(R) == 4 && T >= 3 && T <= 4;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -187,7 +193,7 @@ int default_variant(int dtype, int T) {
         switch (T) {
             case 1: return 5;    // 16x2/3, ring 6
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
-            case 3: return 1;    // 16x2/3, split
+            case 3: return 21;   // 12x3/3, split, running output pointer
             case 4: return 15;   // 8x4/3, split, running output pointer
             default: return 12;  // 8x4/2, split
         }
@@ -195,7 +201,7 @@ int default_variant(int dtype, int T) {
     switch (T) {
         case 1: return 14;       // 16x2/3
         case 2: return 16;       // 8x8/2, two CTAs per SM, split
-        case 3:
+        case 3: return 22;       // 12x6/2, running output pointer
         case 4: return 8;        // 8x8/2, running output pointer
         case 5:
         case 6: return 11;       // 16x2/2, split
@@ -231,7 +237,10 @@ bool is_usable(int v) {
         case 16: return usable<R, T, 16>();
         case 17: return usable<R, T, 17>();
         case 18: return usable<R, T, 18>();
-        default: return usable<R, T, 19>();
+        case 19: return usable<R, T, 19>();
+        case 20: return usable<R, T, 20>();
+        case 21: return usable<R, T, 21>();
+        default: return usable<R, T, 22>();
     }
 }
 
@@ -351,7 +360,10 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 16: return launch_tb_t<R, T, 16>(src, L, a, grid, s);
         case 17: return launch_tb_t<R, T, 17>(src, L, a, grid, s);
         case 18: return launch_tb_t<R, T, 18>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 19>(src, L, a, grid, s);
+        case 19: return launch_tb_t<R, T, 19>(src, L, a, grid, s);
+        case 20: return launch_tb_t<R, T, 20>(src, L, a, grid, s);
+        case 21: return launch_tb_t<R, T, 21>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 22>(src, L, a, grid, s);
     }
 }
 
