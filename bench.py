@@ -336,8 +336,15 @@ def main():
     traffic = None
     tj = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
     key = f"{args.workload}_T{T}_v{args.variant or 0}_n{world}"
+    ncu_evidence = None
     if key in tj:
         traffic = tj[key].get("dram_bytes_per_launch")
+        # per-LUP DRAM bytes and FP64 pipe use of the same kernel (one ncu --set full capture)
+        ncu_evidence = {"dram_bytes_per_lup": round(traffic / (cells_rank * T), 3) if traffic else None,
+                        "algorithmic_bytes_per_lup": round(2 * es / T, 3),
+                        "fp64_pipe_active_pct": tj[key].get("fp64_pipe_active_pct"),
+                        "issue_active_pct": tj[key].get("issue_active_pct"),
+                        "source": tj[key].get("source")}
 
     R_hbm = hbm * T / (2 * es)                      # GLUP/s, HBM term
     R_fp = p_fp64 / 6 / 1e9 if dt == "f64" else float("inf")
@@ -383,7 +390,7 @@ def main():
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "kernel": f"tb_kernel T={T}", "peak_source": hbm_src,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "avg_launch_ms": round(t_pass * 1e3, 3)},
+                         "avg_launch_ms": round(t_pass * 1e3, 3), "ncu": ncu_evidence},
             "temporal_roofline": {"T": T, "R_glups": round(R, 1), "frac": round(value / R, 4),
                                   "R_hbm_glups": round(R_hbm * world, 1),
                                   "R_fp64_glups": round(R_fp * world, 1) if R_fp != float("inf") else None,
