@@ -134,6 +134,7 @@ struct Variant {
     int split;                       // 1: split step barrier (see tb_kernel)
     int zcap = 0;                    // > 0: z-chunks at most this many planes (L2 locality)
     int cl = 1;                      // > 1: y-cooperative thread-block clusters of this size
+    int ls = 1;                      // 2: level-split pipeline over a cluster of two CTAs
 };
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
@@ -161,8 +162,12 @@ constexpr Variant kVariants[] = {
     {12, 3, 2, 1, 8, 1, 1},        // 20: fp64 T=4 alternative (ties 15)
     {12, 3, 3, 1, 8, 1, 1},        // 21: fp64 T=3
     {12, 6, 2, 1, 8, 1, 0, 128},   // 22: fp32 T=3 (64x72 footprint)
+    // level-split pipeline: two CTAs (two SMs) of a cluster apply levels 1..T/2 and T/2+1..T
+    {8, 4, 3, 1, 8, 1, 1, 0, 1, 2},    // 23: 15 per CTA (T=8: 4 levels each)
+    {8, 4, 2, 1, 8, 1, 1, 0, 1, 2},    // 24: 12 per CTA
+    {12, 3, 3, 1, 8, 1, 1, 0, 1, 2},   // 25: 21 per CTA
 };
-constexpr int kNumVariants = 23;
+constexpr int kNumVariants = 26;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
@@ -176,6 +181,7 @@ constexpr bool compiled() {
     if (V == 19) return T == 2;
     if (V == 20 || V == 21) return sizeof(R) == 8 && T >= 3 && T <= 4;
     if (V == 22) return sizeof(R) == 4 && T >= 3 && T <= 4;
+    if (V >= 23 && V <= 25) return T == 4 || T == 6 || T == 8;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -195,6 +201,8 @@ int default_variant(int dtype, int T) {
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
             case 3: return 21;   // 12x3/3, split, running output pointer
             case 4: return 15;   // 8x4/3, split, running output pointer
+            case 6: return 25;   // level split over two CTAs, 12x3/3 each (3 levels per CTA)
+            case 8: return 23;   // level split over two CTAs, 8x4/3 each (4 levels per CTA)
             default: return 12;  // 8x4/2, split
         }
     }
@@ -212,7 +220,13 @@ int default_variant(int dtype, int T) {
 template <typename R, int T, int V>
 constexpr bool usable() {
     constexpr Variant v = kVariants[V];
-    return compiled<R, T, V>() && sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.cl>::FITS;
+    if constexpr (!compiled<R, T, V>()) {
+        return false;
+    } else {
+        // level split: each CTA holds T/ls levels; the footprint still carries the T halo
+        return sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>::FITS &&
+               v.by * v.py * v.cl - 2 * T >= 1;
+    }
 }
 
 template <typename R, int T>
@@ -240,7 +254,10 @@ bool is_usable(int v) {
         case 19: return usable<R, T, 19>();
         case 20: return usable<R, T, 20>();
         case 21: return usable<R, T, 21>();
-        default: return usable<R, T, 22>();
+        case 22: return usable<R, T, 22>();
+        case 23: return usable<R, T, 23>();
+        case 24: return usable<R, T, 24>();
+        default: return usable<R, T, 25>();
     }
 }
 
@@ -272,8 +289,9 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
     } else {
         constexpr Variant v = kVariants[V];
-        using Pl = sp::Plan<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.cl>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER, v.cl>;
+        using Pl = sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>;
+        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER, v.cl,
+                                  v.ls>;
         const size_t smem = Pl::SMEM;
         // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
         static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
@@ -297,13 +315,14 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          SP_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-        if constexpr (v.cl > 1) {
+        if constexpr (v.cl > 1 || v.ls > 1) {
+            constexpr int csize = v.cl > 1 ? v.cl : v.ls;
             // persistent clusters: as many as can be co-resident, round-robin units
             static std::atomic<uint64_t> occ[64] = {};   // per device: active clusters + 1
             cudaLaunchConfig_t cfg = {};
             cudaLaunchAttribute attr[1];
             attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = v.cl;
+            attr[0].val.clusterDim.x = csize;
             attr[0].val.clusterDim.y = 1;
             attr[0].val.clusterDim.z = 1;
             cfg.blockDim = dim3(Pl::NT, 1, 1);
@@ -313,19 +332,19 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
             cfg.numAttrs = 1;
             uint64_t nc = occ[dev & 63].load();
             if (nc == 0) {
-                if (v.cl > 8) SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                if (csize > 8) SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
                 int n = 0;
-                cfg.gridDim = dim3(v.cl * 148, 1, 1);
+                cfg.gridDim = dim3(csize * 148, 1, 1);
                 SP_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
-                if (n < 1) return fail(SP_ERR_DEVICE, "no cluster of %d CTAs fits (variant %d)", v.cl, V);
+                if (n < 1) return fail(SP_ERR_DEVICE, "no cluster of %d CTAs fits (variant %d)", csize, V);
                 nc = (uint64_t)n + 1;
                 occ[dev & 63].store(nc);
                 if (getenv("SP_DEBUG_CLUSTER"))
                     fprintf(stderr, "[sp] variant %d T=%d: %d active clusters of %d CTAs (smem %zu)\n", V, T, n,
-                            v.cl, smem);
+                            csize, smem);
             }
             const int clusters = (int)std::min<int64_t>(a.units, (int64_t)(nc - 1));
-            cfg.gridDim = dim3(clusters * v.cl, 1, 1);
+            cfg.gridDim = dim3(clusters * csize, 1, 1);
             SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a));
         } else {
             kern<<<grid, Pl::NT, smem, stream>>>(map, a);
@@ -363,7 +382,10 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 19: return launch_tb_t<R, T, 19>(src, L, a, grid, s);
         case 20: return launch_tb_t<R, T, 20>(src, L, a, grid, s);
         case 21: return launch_tb_t<R, T, 21>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 22>(src, L, a, grid, s);
+        case 22: return launch_tb_t<R, T, 22>(src, L, a, grid, s);
+        case 23: return launch_tb_t<R, T, 23>(src, L, a, grid, s);
+        case 24: return launch_tb_t<R, T, 24>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 25>(src, L, a, grid, s);
     }
 }
 
@@ -801,7 +823,8 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     a.gz = (int)L->gz;
     const int64_t nzb = out_hi[0] - out_lo[0];
     const int64_t tiles = (int64_t)a.ntx * a.nty;
-    const int slots = std::max(1, di.sms * kVariants[variant].minb / cl);   // concurrent units
+    const int ls = kVariants[variant].ls;
+    const int slots = std::max(1, di.sms * kVariants[variant].minb / (cl * ls));   // concurrent units
     // z-chunking: minimise waves * (chunk + 2T) -- the wave-quantised cost of
     // every unit streaming chunk+2T planes.
     // Short chunks keep the units in flight close in z, so neighbouring
@@ -828,7 +851,7 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     a.units = (int)(tiles * nch);
     a.strip = g_strip;
     a.sched = nullptr;
-    if (g_dynamic && cl == 1) {
+    if (g_dynamic && cl == 1 && ls == 1) {
         rc = sched_counter(&a.sched);
         if (rc) return rc;
     }

@@ -144,6 +144,28 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
     } while (!ok);
 }
 
+// remote arrive with the default (release.cta) semantics: a WAR release only
+// (the arriving CTA has finished reading; no data is published by it)
+__device__ __forceinline__ void mbar_arrive_remote_cta(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// 16-byte (fp64) / 8-byte (fp32) asynchronous store into another CTA's shared
+// memory that completes `bytes` of transaction on that CTA's mbarrier
+template <typename R> struct StAsync;
+template <> struct StAsync<double> {
+    __device__ static __forceinline__ void v2(uint32_t addr, double x, double y, uint32_t mbar) {
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                     ::"r"(addr), "d"(x), "d"(y), "r"(mbar) : "memory");
+    }
+};
+template <> struct StAsync<float> {
+    __device__ static __forceinline__ void v2(uint32_t addr, float x, float y, uint32_t mbar) {
+        asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];"
+                     ::"r"(addr), "f"(x), "f"(y), "r"(mbar) : "memory");
+    }
+};
+
 template <typename R> struct SmemLd;
 template <> struct SmemLd<double> {
     __device__ static __forceinline__ double2 v2(const void* p) {
@@ -245,7 +267,8 @@ __device__ __forceinline__ int footprint_x(const TBArgs& a, int x0, int T) {
 // Shared-memory plan per instantiation: a RING-deep TMA ring of level-0
 // planes plus, for levels 1..T-1, one plane each -- double-buffered when it
 // fits (one barrier per step), single-buffered otherwise (two barriers).
-template <typename R, int T, int BY, int PY, int SLOTS = 3, int MINB = 1, int RCAP = 8, int CL = 1>
+template <typename R, int T, int BY, int PY, int SLOTS = 3, int MINB = 1, int RCAP = 8, int CL = 1,
+          int LS = 1>
 struct Plan {
     // SLOTS == 1 keeps only v[p] in registers; v[p-1] is re-read from the
     // double-buffered level plane (and ring slot k-2) just before it is
@@ -263,7 +286,7 @@ struct Plan {
     static constexpr int RPLANE = WX * RROWS;
     static constexpr int RPLANE_BYTES = RPLANE * (int)sizeof(R);
     // opt-in smem per CTA (MINB CTAs share the SM's 228 KB), minus barriers
-    static constexpr int BUDGET = (MINB == 1 ? 232448 : 233472 / MINB - 1024) - 256;
+    static constexpr int BUDGET = (MINB == 1 ? 232448 : 233472 / MINB - 1024) - 256 - (LS > 1 ? 128 : 0);
     static constexpr int NL = (T > 1) ? (T - 1) : 0;        // stored level planes
     static constexpr bool DB = 2 * NL * PLANE_BYTES + 3 * RPLANE_BYTES <= BUDGET;
     static constexpr int NBUF = DB ? 2 : 1;
@@ -273,8 +296,11 @@ struct Plan {
     static constexpr bool FITS = RING >= MIN_RING && CL * WY - 2 * T >= 1 && (SLOTS != 1 || DB) &&
                                  (CL == 1 || (DB && SLOTS != 1 && T >= 2));
     static constexpr int NUID = 16;   // unit ids handed from the producer to the consumers
-    static constexpr size_t SMEM =
-        (size_t)RING * RPLANE_BYTES + (size_t)NBUF * NL * PLANE_BYTES + (RING + 2) * 8 + NUID * 4;
+    // LS > 1: T here is the depth one CTA holds; RING more mbarriers ("slot
+    // consumed" of the next CTA's ring)
+    static constexpr int NEMPTY = LS > 1 ? RING : 0;
+    static constexpr size_t SMEM = (size_t)RING * RPLANE_BYTES + (size_t)NBUF * NL * PLANE_BYTES +
+                                   (RING + 2 + NEMPTY) * 8 + NUID * 4;
 };
 
 // CL > 1 (y-cooperative clusters): CL CTAs of a cluster own CL vertically
@@ -284,15 +310,29 @@ struct Plan {
 // paid once per cluster footprint, not per CTA.  The split step barrier
 // spans the cluster: each CTA's edge warps also arrive on the neighbour
 // CTA's step barrier.  Units are assigned round-robin per cluster.
+//
+// LS = 2 (level-split pipeline, the paper's pipelined temporal blocking
+// mapped onto a cluster of two CTAs on two SMs; R/pipeline.py:395-408): both
+// CTAs march the same footprint (halo T) through z; rank 0 applies levels
+// 1..D (D = T/2) to the TMA-fed level-0 planes and, instead of storing level
+// D, pushes each finished level-D plane into rank 1's ring with st.async
+// (complete_tx on rank 1's slot barrier, like a TMA load); rank 1 applies
+// levels D+1..T to that stream and stores level T.  Rank 1 hands each ring
+// slot back through a remote arrive on rank 0's "consumed" barrier.  Each
+// CTA keeps only D levels of z-queue in registers, so T=8 fits where one CTA
+// holding all eight levels spills.
 template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV,
-          bool PEER = false, int CL = 1>
+          bool PEER = false, int CL = 1, int LS = 1>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
+    static_assert(LS == 1 || (LS == 2 && T % 2 == 0 && CL == 1 && !PEER && SLOTS != 1),
+                  "level split: two CTAs, even depth");
+    constexpr int D = T / LS;                    // levels this CTA applies
     constexpr int QN = SLOTS == 1 ? 2 : SLOTS;   // register slots per level
     using A = Arith<R>;
     using V2 = typename A::V2;
-    using P = Plan<R, T, BY, PY, SLOTS, MINB, RCAP, CL>;
+    using P = Plan<R, D, BY, PY, SLOTS, MINB, RCAP, CL, LS>;
     constexpr int WY = P::WY;
     constexpr int PLANE = P::PLANE;
     constexpr int RPLANE = P::RPLANE;
@@ -306,14 +346,15 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     R* lvl = ring + RING_N * RPLANE;  // [level-1][buf] planes for levels 1..T-1
     uint64_t* full = reinterpret_cast<uint64_t*>(lvl + P::NBUF * P::NL * PLANE);
     uint64_t* lbar = full + RING_N;   // [2]: step-parity barriers of the level planes (SPLIT)
-    volatile int* uid = reinterpret_cast<volatile int*>(lbar + 2);
+    uint64_t* empty = lbar + 2;       // [NEMPTY] (LS > 1, rank 0): rank 1 consumed ring slot i
+    volatile int* uid = reinterpret_cast<volatile int*>(empty + P::NEMPTY);
     // SPLIT: instead of one __syncthreads per z-step, each warp arrives on
     // lbar[step & 1] when it has finished the step, and waits for the
     // previous step's arrivals only where it first touches the level planes
     // (the level-1 edge-row store).  The TMA wait, ring loads and level-1
     // arithmetic of step k overlap the slowest warps of step k-1; thread 0
     // refills the ring slot freed by step k-1 right after that wait.
-    constexpr bool SPLIT = SPLITV && T >= 2 && P::DB;
+    constexpr bool SPLIT = SPLITV && D >= 2 && P::DB;
 
     const int lane = threadIdx.x & 31;
     const int wy = threadIdx.x >> 5;
@@ -325,16 +366,28 @@ __global__ void __launch_bounds__(32 * BY, MINB)
 
     const int crank = CL > 1 ? (int)cluster_rank() : 0;
     const bool has_up = CL > 1 && crank > 0, has_dn = CL > 1 && crank < CL - 1;
+    // level split: this CTA's first level is L0+1; Te = levels from there to T
+    // (its input planes are those of level L0, which start Te planes before the chunk)
+    const int lrank = LS > 1 ? (int)cluster_rank() : 0;
+    const int L0 = lrank * D, Te = T - L0;
     if (threadIdx.x == 0) {
         for (int i = 0; i < RING_N; ++i) mbar_init(&full[i], 1);
+        for (int i = 0; i < P::NEMPTY; ++i) mbar_init(&empty[i], 1);
         // own warps, plus the neighbour CTAs' edge warps that read/write our edge rows
         const uint32_t nb = BY + (has_up ? 1 : 0) + (has_dn ? 1 : 0);
         mbar_init(&lbar[0], nb);
         mbar_init(&lbar[1], nb);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if constexpr (CL > 1) cluster_sync_all();   // neighbours' barriers exist before any remote arrive
+    if constexpr (CL > 1 || LS > 1) cluster_sync_all();   // remote barriers exist before any remote arrive
     else __syncthreads();
+    // LS > 1: rank 0 stores into rank 1's ring and completes rank 1's slot
+    // barriers; rank 1 arrives on rank 0's "consumed" barriers
+    uint32_t nx_ring = 0, nx_full = 0, pv_empty = 0;
+    if constexpr (LS > 1) {
+        if (lrank == 0) { nx_ring = map_rank(ring, 1); nx_full = map_rank(full, 1); }
+        else pv_empty = map_rank(empty, 0);
+    }
     // DSMEM addresses of the neighbour slices' step barriers and level planes
     uint32_t up_lbar = 0, dn_lbar = 0, up_lvl = 0, dn_lvl = 0;
     if constexpr (CL > 1) {
@@ -352,7 +405,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     int pu = -1, pseq = 0, pc0 = 0, pc1 = 0, pc2 = 0, pc2_end = 0;
     bool pdone = false;
     auto producer_unit = [&]() {
-        if constexpr (CL > 1) {
+        if constexpr (CL > 1 || LS > 1) {
             pu = pseq == 0 ? (int)cluster_id_x() : pu + (int)cluster_count_x();
         } else if (a.sched) {
             pu = (int)atomicAdd(a.sched, 1u);
@@ -366,8 +419,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         const Unit pw = decode_unit(a, pu);
         pc0 = footprint_x<R>(a, pw.x0, T) + a.x_off;
         pc1 = pw.y0 - T + crank * WY - HR + a.gy;
-        pc2 = pw.zc0 - T + a.gz;
-        pc2_end = pw.zc1 + T + a.gz;
+        pc2 = pw.zc0 - Te + a.gz;
+        pc2_end = pw.zc1 + Te + a.gz;
     };
     if (threadIdx.x == 0) producer_unit();
     auto produce = [&](int slot) {
@@ -377,7 +430,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             return;
         }
         mbar_expect_tx(&full[slot], kRingBytes);
-        tma_load_3d(ring + slot * RPLANE, &tmap, &full[slot], pc0, pc1, pc2);
+        if (LS == 1 || lrank == 0) tma_load_3d(ring + slot * RPLANE, &tmap, &full[slot], pc0, pc1, pc2);
+        else mbar_arrive_remote_cta(pv_empty + 8u * slot);   // rank 0 may fill this slot
         if (++pc2 == pc2_end) producer_unit();
     };
     if (threadIdx.x == 0) {
@@ -388,6 +442,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
 
     const R sixth = A::sixth();
     uint32_t gstep = 0;
+    uint32_t gsent = 0;   // LS > 1, rank 0: level-D planes pushed to rank 1 so far
 
     for (int cseq = 0;; ++cseq) {
         // the unit's first plane (or the end marker) has landed: its id is published
@@ -396,19 +451,20 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         if (u < 0) break;
         const Unit w = decode_unit(a, u);
         const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T + crank * WY;
-        const int nsteps = (w.zc1 - w.zc0) + 2 * T;
+        const int nsteps = (w.zc1 - w.zc0) + 2 * Te;
 
         // Per-level x/y domain of this thread's columns: x bits (PX per level)
         // and y bits (PY per level); `fastm` bit t-1 = every cell of this
         // WARP lies in level t's x/y domain (then the Dirichlet select is
         // skipped warp-uniformly).
         uint32_t xin = 0;
-        uint64_t yin = 0;   // T*PY bits (up to 64)
+        uint64_t yin = 0;   // D*PY bits (up to 64)
         uint32_t fastm = 0;
 #pragma unroll
-        for (int t = 1; t <= T; ++t) {
-            int xl = a.lo[2] - a.elo[2] * (T - t), xh = a.hi[2] + a.ehi[2] * (T - t);
-            int yl = a.lo[1] - a.elo[1] * (T - t), yh = a.hi[1] + a.ehi[1] * (T - t);
+        for (int t = 1; t <= D; ++t) {
+            const int ext = T - L0 - t;   // level L0+t's domain extension
+            int xl = a.lo[2] - a.elo[2] * ext, xh = a.hi[2] + a.ehi[2] * ext;
+            int yl = a.lo[1] - a.elo[1] * ext, yh = a.hi[1] + a.ehi[1] * ext;
             bool all = true;
 #pragma unroll
             for (int i = 0; i < PX; ++i) {
@@ -440,7 +496,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         }
         R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
         const int64_t pz = a.pz, py = a.py;
-        R* dnext = dcol + (int64_t)(w.zc0 - 2 * T) * pz;   // plane q-T of step 0
+        R* dnext = dcol + (int64_t)(w.zc0 - Te - D) * pz;   // plane q-D of step 0
         // both x cells written and the pair 16-byte aligned (same for every row: py is)
         const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
         // every row of the patch is written with one 16-byte store (interior tiles)
@@ -454,11 +510,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         // queue shifts by moves (fewer live registers, more instructions).
         // SLOTS == 1: Q[f] = v[p] and Q[f^1] = v[p+1] (new), steps unrolled by 2;
         // v[p-1] comes back from shared memory.
-        R Q[QN][T][PY][PX];
+        R Q[QN][D][PY][PX];
 #pragma unroll
         for (int f = 0; f < QN; ++f)
 #pragma unroll
-            for (int t = 0; t < T; ++t)
+            for (int t = 0; t < D; ++t)
 #pragma unroll
                 for (int j = 0; j < PY; ++j)
 #pragma unroll
@@ -480,12 +536,12 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             const int pslot2 = (gstep + RING_N - 2) % RING_N;
             const int cur = P::DB ? (int)(gstep & 1u) : 0;
             const int prv = P::DB ? cur ^ 1 : 0;
-            const int q = w.zc0 - T + st;
+            const int q = w.zc0 - Te + st;
 
             // s_t = (x- + x+) + (y- + y+) of level t-1 at plane q-t, produced in
             // the previous step (ring slot pslot / level buffer prv; own and
             // lane-neighbour cells from the registers of Q[F1]).
-            R s[T][PY][PX];
+            R s[D][PY][PX];
             auto xy_sums = [&](int t) {
                 const R* Pl = (t == 1) ? ring + pslot * RPLANE + HR * WX
                                        : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
@@ -519,13 +575,13 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             };
             if constexpr (!P::DB) {
 #pragma unroll
-                for (int t = 1; t <= T; ++t) xy_sums(t);
+                for (int t = 1; t <= D; ++t) xy_sums(t);
                 __syncthreads();   // single buffers: all reads before any overwrite
             }
 
             mbar_wait(&full[slot], (gstep / RING_N) & 1);
             // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
-            R Nt[SLOTS == 2 ? T : 1][PY][PX];
+            R Nt[SLOTS == 2 ? D : 1][PY][PX];
             auto newv = [&](int t) -> R(&)[PY][PX] {
                 if constexpr (SLOTS != 2) return Q[F2][t];
                 else return Nt[t];
@@ -551,9 +607,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     n0[j][1] = r.y;
                 }
             }
-            R out[PY][PX];  // level-T values of plane q-T
+            R out[PY][PX];  // level-D values of plane q-D
 #pragma unroll
-            for (int t = 1; t <= T; ++t) {
+            for (int t = 1; t <= D; ++t) {
                 if constexpr (P::DB) xy_sums(t);
                 const R(&mm)[PY][PX] = *([&]() -> const R(*)[PY][PX] {
                     if constexpr (SLOTS == 1) return &mv;
@@ -561,11 +617,12 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 }());
                 const R(&cc)[PY][PX] = Q[F1][t - 1];
                 const R(&nn)[PY][PX] = newv(t - 1);
-                R(&dst)[PY][PX] = (t < T) ? newv(t < T ? t : 0) : out;
+                R(&dst)[PY][PX] = (t < D) ? newv(t < D ? t : 0) : out;
                 uint32_t inm = 0;   // SLOW: one bit per cell, in D_t this step
                 if constexpr (!FAST) {
                     const int p = q - t;
-                    const bool zin = p >= a.lo[0] - a.elo[0] * (T - t) && p < a.hi[0] + a.ehi[0] * (T - t);
+                    const int ext = T - L0 - t;
+                    const bool zin = p >= a.lo[0] - a.elo[0] * ext && p < a.hi[0] + a.ehi[0] * ext;
                     const uint32_t xb = (xin >> ((t - 1) * PX)) & ((1u << PX) - 1);
                     const uint32_t yb = (uint32_t)(yin >> ((t - 1) * PY)) & ((1u << PY) - 1);
 #pragma unroll
@@ -600,7 +657,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                         produce(SLOTS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
                     }
                 }
-                if (t < T) {
+                if (t < D) {
                     R* Pl = lvl + ((t - 1) * P::NBUF + cur) * PLANE;
                     if constexpr (SLOTS == 1) {
                         // this buffer still holds level t at plane q-t-1 = v[p-1]
@@ -627,8 +684,17 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             // advances one plane per step; otherwise the address is formed per
             // step.  Both are bit-identical -- ptxas schedules them differently
             // and the tuned variant table picks per (dtype, T).
-            if (st >= 2 * T) {
-                R* d = RSTORE ? dnext : dcol + (int64_t)(q - T) * pz;
+            if (LS > 1 && lrank == 0 && st >= 2 * D) {
+                // level D of plane q-D -> rank 1's ring, once rank 1 has freed the slot
+                const uint32_t s1 = gsent % RING_N;
+                mbar_wait(&empty[s1], (gsent / RING_N) & 1);
+                const uint32_t base = nx_ring + (uint32_t)((s1 * RPLANE + cy * WX + cx) * sizeof(R));
+#pragma unroll
+                for (int j = 0; j < PY; ++j)
+                    StAsync<R>::v2(base + (uint32_t)(j * WX * sizeof(R)), out[j][0], out[j][1], nx_full + 8u * s1);
+                ++gsent;
+            } else if (st >= 2 * D) {
+                R* d = RSTORE ? dnext : dcol + (int64_t)(q - D) * pz;
                 auto put = [&](R* b) {
                     if (full_rows) {
 #pragma unroll
@@ -650,7 +716,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 };
                 put(d);
                 if constexpr (PEER) {   // the same plane into a neighbour's ghost plane
-                    const int p = q - T;
+                    const int p = q - D;
                     if (p < a.rz_lo) put(d + a.rd_lo);
                     if (p >= a.rz_hi) put(d + a.rd_hi);
                 }
@@ -677,11 +743,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             ++gstep;
         };
         // warp-uniform: the whole warp is inside every level's x/y domain
-        const bool fast_xy = fastm == (1u << T) - 1u;
+        const bool fast_xy = fastm == (1u << D) - 1u;
         // planes q-t of every level inside its z domain
         auto zin_all = [&](int st) {
-            const int q = w.zc0 - T + st;
-            return q - 1 < a.hi[0] + a.ehi[0] * (T - 1) && q - T >= a.lo[0];
+            const int q = w.zc0 - Te + st;
+            return q - 1 < a.hi[0] + a.ehi[0] * (T - L0 - 1) && q - D >= a.lo[0];
         };
         auto run = [&](auto phase, int st) {
             if (fast_xy && zin_all(st)) step(phase, std::true_type{}, st);
@@ -704,7 +770,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         }
     }
     // no CTA leaves while a neighbour may still read its planes or arrive on its barriers
-    if constexpr (CL > 1) cluster_sync_all();
+    if constexpr (CL > 1 || LS > 1) cluster_sync_all();
 }
 
 // ---- K1: single-level streaming sweep ---------------------------------------

@@ -299,7 +299,7 @@ def test_c1_full_grid_vs_reference(sp, kat, ref_fields):
     assert bitwise(inner[kat["c1_planes_index"]], ref_fields["c1_planes_l100"])
 
 
-@pytest.mark.parametrize("shape_id", list(range(1, 24)))
+@pytest.mark.parametrize("shape_id", list(range(1, 27)))
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_every_cta_shape(sp, O, shape_id, dtype):
     lib = sp._native.lib()
@@ -425,3 +425,24 @@ def test_upload_download_round_trip(sp, O, dtype):
     assert bitwise(g.download().numpy(), ref.interior())     # fresh pinned tensor, synchronised
     with pytest.raises(sp.GridError):
         g.upload(np.zeros((3, 3, 3), dtype=dtype))
+
+
+@pytest.mark.parametrize("shape_id", [24, 25, 26])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_level_split_pipeline(sp, O, shape_id, dtype):
+    """Level-split K2 (levels 1..T/2 on one CTA, T/2+1..T on its cluster peer, planes handed
+    over by st.async): ragged boxes with walls, depths 4/6/8, and sub-box output passes."""
+    lib = sp._native.lib()
+    lib.sp_set_tuning(shape_id, 0)
+    try:
+        for shape, levels, depth in [((37, 45, 70), 16, 8), ((23, 40, 66), 12, 6), ((30, 33, 129), 8, 4),
+                                     ((9, 17, 20), 8, 8)]:
+            faces = (0.7, -0.25, 1.5, 0.0, -1.0, 0.5)
+            seed = sum(shape) + depth
+            g = sp.TwoGrid(dims_of(sp, shape), sp.FillPattern.dirichlet_box("random", shape, faces, seed=seed),
+                           dtype=dtype)
+            sp.sweeps(g, levels, depth=depth)
+            ref = oracle_run(O, shape, "random", seed, faces, levels, dtype=dtype)
+            assert bitwise(g.interior(), ref.interior()), (shape_id, shape, depth)
+    finally:
+        lib.sp_set_tuning(0, 0)
