@@ -166,8 +166,9 @@ constexpr Variant kVariants[] = {
     {8, 4, 3, 1, 8, 1, 1, 0, 1, 2},    // 23: 15 per CTA (T=8: 4 levels each)
     {8, 4, 2, 1, 8, 1, 1, 0, 1, 2},    // 24: 12 per CTA
     {12, 3, 3, 1, 8, 1, 1, 0, 1, 2},   // 25: 21 per CTA
+    {8, 8, 2, 1, 8, 1, 1, 0, 1, 4},    // 26: 64x64 footprint, chain of four CTAs (T=8: 2 levels each)
 };
-constexpr int kNumVariants = 26;
+constexpr int kNumVariants = 27;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
@@ -182,6 +183,7 @@ constexpr bool compiled() {
     if (V == 20 || V == 21) return sizeof(R) == 8 && T >= 3 && T <= 4;
     if (V == 22) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V >= 23 && V <= 25) return T == 4 || T == 6 || T == 8;
+    if (V == 26) return T == 8;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -257,7 +259,8 @@ bool is_usable(int v) {
         case 22: return usable<R, T, 22>();
         case 23: return usable<R, T, 23>();
         case 24: return usable<R, T, 24>();
-        default: return usable<R, T, 25>();
+        case 25: return usable<R, T, 25>();
+        default: return usable<R, T, 26>();
     }
 }
 
@@ -385,7 +388,8 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 22: return launch_tb_t<R, T, 22>(src, L, a, grid, s);
         case 23: return launch_tb_t<R, T, 23>(src, L, a, grid, s);
         case 24: return launch_tb_t<R, T, 24>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 25>(src, L, a, grid, s);
+        case 25: return launch_tb_t<R, T, 25>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 26>(src, L, a, grid, s);
     }
 }
 

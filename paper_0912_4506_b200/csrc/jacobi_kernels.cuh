@@ -326,8 +326,8 @@ template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int 
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
-    static_assert(LS == 1 || (LS == 2 && T % 2 == 0 && CL == 1 && !PEER && SLOTS != 1),
-                  "level split: two CTAs, even depth");
+    static_assert(LS == 1 || (T % LS == 0 && CL == 1 && !PEER && SLOTS != 1),
+                  "level split: depth a multiple of the cluster size");
     constexpr int D = T / LS;                    // levels this CTA applies
     constexpr int QN = SLOTS == 1 ? 2 : SLOTS;   // register slots per level
     using A = Arith<R>;
@@ -370,6 +370,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     // (its input planes are those of level L0, which start Te planes before the chunk)
     const int lrank = LS > 1 ? (int)cluster_rank() : 0;
     const int L0 = lrank * D, Te = T - L0;
+    const bool first = lrank == 0, last = lrank == LS - 1;   // TMA-fed / storing to HBM
     if (threadIdx.x == 0) {
         for (int i = 0; i < RING_N; ++i) mbar_init(&full[i], 1);
         for (int i = 0; i < P::NEMPTY; ++i) mbar_init(&empty[i], 1);
@@ -381,12 +382,12 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     }
     if constexpr (CL > 1 || LS > 1) cluster_sync_all();   // remote barriers exist before any remote arrive
     else __syncthreads();
-    // LS > 1: rank 0 stores into rank 1's ring and completes rank 1's slot
-    // barriers; rank 1 arrives on rank 0's "consumed" barriers
+    // LS > 1: rank r stores into rank r+1's ring and completes its slot
+    // barriers; rank r+1 arrives on rank r's "consumed" barriers
     uint32_t nx_ring = 0, nx_full = 0, pv_empty = 0;
     if constexpr (LS > 1) {
-        if (lrank == 0) { nx_ring = map_rank(ring, 1); nx_full = map_rank(full, 1); }
-        else pv_empty = map_rank(empty, 0);
+        if (!last) { nx_ring = map_rank(ring, lrank + 1); nx_full = map_rank(full, lrank + 1); }
+        if (!first) pv_empty = map_rank(empty, lrank - 1);
     }
     // DSMEM addresses of the neighbour slices' step barriers and level planes
     uint32_t up_lbar = 0, dn_lbar = 0, up_lvl = 0, dn_lvl = 0;
@@ -430,8 +431,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             return;
         }
         mbar_expect_tx(&full[slot], kRingBytes);
-        if (LS == 1 || lrank == 0) tma_load_3d(ring + slot * RPLANE, &tmap, &full[slot], pc0, pc1, pc2);
-        else mbar_arrive_remote_cta(pv_empty + 8u * slot);   // rank 0 may fill this slot
+        if (LS == 1 || first) tma_load_3d(ring + slot * RPLANE, &tmap, &full[slot], pc0, pc1, pc2);
+        else mbar_arrive_remote_cta(pv_empty + 8u * slot);   // rank r-1 may fill this slot
         if (++pc2 == pc2_end) producer_unit();
     };
     if (threadIdx.x == 0) {
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
 
     const R sixth = A::sixth();
     uint32_t gstep = 0;
-    uint32_t gsent = 0;   // LS > 1, rank 0: level-D planes pushed to rank 1 so far
+    uint32_t gsent = 0;   // LS > 1, not last: planes pushed to the next rank so far
 
     for (int cseq = 0;; ++cseq) {
         // the unit's first plane (or the end marker) has landed: its id is published
@@ -684,8 +685,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             // advances one plane per step; otherwise the address is formed per
             // step.  Both are bit-identical -- ptxas schedules them differently
             // and the tuned variant table picks per (dtype, T).
-            if (LS > 1 && lrank == 0 && st >= 2 * D) {
-                // level D of plane q-D -> rank 1's ring, once rank 1 has freed the slot
+            if (LS > 1 && !last && st >= 2 * D) {
+                // level L0+D of plane q-D -> the next rank's ring, once it has freed the slot
                 const uint32_t s1 = gsent % RING_N;
                 mbar_wait(&empty[s1], (gsent / RING_N) & 1);
                 const uint32_t base = nx_ring + (uint32_t)((s1 * RPLANE + cy * WX + cx) * sizeof(R));

@@ -299,7 +299,7 @@ def test_c1_full_grid_vs_reference(sp, kat, ref_fields):
     assert bitwise(inner[kat["c1_planes_index"]], ref_fields["c1_planes_l100"])
 
 
-@pytest.mark.parametrize("shape_id", list(range(1, 27)))
+@pytest.mark.parametrize("shape_id", list(range(1, 28)))
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_every_cta_shape(sp, O, shape_id, dtype):
     lib = sp._native.lib()
@@ -427,7 +427,7 @@ def test_upload_download_round_trip(sp, O, dtype):
         g.upload(np.zeros((3, 3, 3), dtype=dtype))
 
 
-@pytest.mark.parametrize("shape_id", [24, 25, 26])
+@pytest.mark.parametrize("shape_id", [24, 25, 26, 27])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_level_split_pipeline(sp, O, shape_id, dtype):
     """Level-split K2 (levels 1..T/2 on one CTA, T/2+1..T on its cluster peer, planes handed
