@@ -19,6 +19,14 @@
 // in the reference's summation order (R/kernel.py:27-34), with explicit
 // __dadd_rn/__dmul_rn (no FMA contraction) -> bit-identical to numpy.
 //
+// Cluster forms of K2 (template parameters, see the comment above tb_kernel):
+//   LS > 1 -- level-split pipeline: LS CTAs of a cluster each apply T/LS of
+//             the levels to the same footprint, handing finished planes to
+//             the next CTA's ring with st.async (the paper's pipelined
+//             temporal blocking; the fp64 T=6/8 defaults);
+//   CL > 1 -- y-cooperative slices sharing edge rows over DSMEM (measured
+//             slower; kept as tested variants).
+//
 // K1 (a single level over any box, R/kernel.py:37-40) is tb_kernel<R,1,...>.
 // K3 `fill_kernel` initialises a grid from the coordinate hash
 // (R/grid.py:54-118).  K5 `digest_kernel` reduces the interior to the 64-bit
