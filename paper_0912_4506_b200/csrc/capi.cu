@@ -167,8 +167,10 @@ constexpr Variant kVariants[] = {
     {8, 4, 2, 1, 8, 1, 1, 0, 1, 2},    // 24: 12 per CTA
     {12, 3, 3, 1, 8, 1, 1, 0, 1, 2},   // 25: 21 per CTA
     {8, 8, 2, 1, 8, 1, 1, 0, 1, 4},    // 26: 64x64 footprint, chain of four CTAs (T=8: 2 levels each)
+    // slots 4: level 0 re-read from the ring into step-parity registers (no level-0 moves)
+    {8, 4, 4, 1, 8, 0, 1},         // 27: fp64 T=5: 12 with slots 4
 };
-constexpr int kNumVariants = 27;
+constexpr int kNumVariants = 28;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 int g_variant_override = -1;
 
@@ -184,6 +186,7 @@ constexpr bool compiled() {
     if (V == 22) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V >= 23 && V <= 25) return T == 4 || T == 6 || T == 8;
     if (V == 26) return T == 8;
+    if (V == 27) return sizeof(R) == 8 && T >= 4 && T <= 5;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -203,6 +206,7 @@ int default_variant(int dtype, int T) {
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
             case 3: return 21;   // 12x3/3, split, running output pointer
             case 4: return 15;   // 8x4/3, split, running output pointer
+            case 5: return 27;   // 8x4, level 0 re-read from the ring (slots 4), split
             case 6: return 25;   // level split over two CTAs, 12x3/3 each (3 levels per CTA)
             case 8: return 23;   // level split over two CTAs, 8x4/3 each (4 levels per CTA)
             default: return 12;  // 8x4/2, split
@@ -260,7 +264,8 @@ bool is_usable(int v) {
         case 23: return usable<R, T, 23>();
         case 24: return usable<R, T, 24>();
         case 25: return usable<R, T, 25>();
-        default: return usable<R, T, 26>();
+        case 26: return usable<R, T, 26>();
+        default: return usable<R, T, 27>();
     }
 }
 
@@ -389,7 +394,8 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 23: return launch_tb_t<R, T, 23>(src, L, a, grid, s);
         case 24: return launch_tb_t<R, T, 24>(src, L, a, grid, s);
         case 25: return launch_tb_t<R, T, 25>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 26>(src, L, a, grid, s);
+        case 26: return launch_tb_t<R, T, 26>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 27>(src, L, a, grid, s);
     }
 }
 

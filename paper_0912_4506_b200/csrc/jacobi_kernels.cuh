@@ -333,11 +333,17 @@ template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int 
           bool PEER = false, int CL = 1, int LS = 1>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
-    static_assert(SLOTS >= 1 && SLOTS <= 3, "z-queue slots");
-    static_assert(LS == 1 || (T % LS == 0 && CL == 1 && !PEER && SLOTS != 1),
+    // SLOTS = 4: levels >= 1 as SLOTS = 2; level 0's v[p] is re-read from the
+    // ring every step into one of two register sets that alternate with the
+    // step parity (the set loaded in step k is v[p-1] in step k+1), so level
+    // 0 needs no queue moves.
+    constexpr bool L0C = SLOTS == 4;
+    constexpr int QS = L0C ? 2 : SLOTS;
+    static_assert(SLOTS >= 1 && SLOTS <= 4, "z-queue slots");
+    static_assert(LS == 1 || (T % LS == 0 && CL == 1 && !PEER && QS != 1),
                   "level split: depth a multiple of the cluster size");
     constexpr int D = T / LS;                    // levels this CTA applies
-    constexpr int QN = SLOTS == 1 ? 2 : SLOTS;   // register slots per level
+    constexpr int QN = QS == 1 ? 2 : QS;         // register slots per level
     using A = Arith<R>;
     using V2 = typename A::V2;
     using P = Plan<R, D, BY, PY, SLOTS, MINB, RCAP, CL, LS>;
@@ -346,7 +352,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     constexpr int RPLANE = P::RPLANE;
     constexpr int HR = P::HR;
     constexpr int RING_N = P::RING;
-    static_assert(CL == 1 || (SPLITV && P::DB && SLOTS != 1 && T >= 2 && !PEER),
+    static_assert(CL == 1 || (SPLITV && P::DB && QS != 1 && T >= 2 && !PEER),
                   "cluster variants need the split barrier, double-buffered planes, 2-3 slots");
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -446,7 +452,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
         // the slot released after step k is k-1 (k-2 with SLOTS == 1): prime the rest
-        for (int i = 0; i < RING_N - (SLOTS == 1 ? 2 : 1); ++i) produce(i);
+        for (int i = 0; i < RING_N - (QS == 1 ? 2 : 1); ++i) produce(i);
     }
 
     const R sixth = A::sixth();
@@ -520,6 +526,13 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         // SLOTS == 1: Q[f] = v[p] and Q[f^1] = v[p+1] (new), steps unrolled by 2;
         // v[p-1] comes back from shared memory.
         R Q[QN][D][PY][PX];
+        R M0[L0C ? 2 : 1][PY][PX];   // L0C: level 0's v[p-1] / v[p] by step parity
+#pragma unroll
+        for (int f = 0; f < (L0C ? 2 : 1); ++f)
+#pragma unroll
+            for (int j = 0; j < PY; ++j)
+#pragma unroll
+                for (int i = 0; i < PX; ++i) M0[f][j][i] = R(0);
 #pragma unroll
         for (int f = 0; f < QN; ++f)
 #pragma unroll
@@ -535,9 +548,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         // value (Dirichlet walls, rank faces) through a per-cell select.
         auto step = [&](auto phase, auto fast, int st) {
             constexpr int PH = decltype(phase)::value;
-            constexpr int F0 = SLOTS == 3 ? PH : 0;                                   // v[p-1]
-            constexpr int F1 = SLOTS == 3 ? (PH + 1) % 3 : (SLOTS == 1 ? PH : 1);    // v[p]
-            constexpr int F2 = SLOTS == 3 ? (PH + 2) % 3 : (SLOTS == 1 ? PH ^ 1 : 0); // v[p+1]
+            constexpr int F0 = QS == 3 ? PH : 0;                               // v[p-1]
+            constexpr int F1 = QS == 3 ? (PH + 1) % 3 : (QS == 1 ? PH : 1);    // v[p]
+            constexpr int F2 = QS == 3 ? (PH + 2) % 3 : (QS == 1 ? PH ^ 1 : 0); // v[p+1]
+            // L0C: this step's level-0 v[p] lands in M0[PH ^ 1]; M0[PH] is v[p-1]
+            constexpr int C0 = L0C ? (PH ^ 1) : 0, M0I = L0C ? PH : 0;
             constexpr bool FAST = decltype(fast)::value;
 
             const int slot = gstep % RING_N;
@@ -546,6 +561,19 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             const int cur = P::DB ? (int)(gstep & 1u) : 0;
             const int prv = P::DB ? cur ^ 1 : 0;
             const int q = w.zc0 - Te + st;
+            if constexpr (L0C) {   // level 0 at plane q-1 (ring slot of the previous step)
+                const R* Lc = ring + pslot * RPLANE + HR * WX;
+#pragma unroll
+                for (int j = 0; j < PY; ++j) {
+                    V2 r = *reinterpret_cast<const V2*>(Lc + (cy + j) * WX + cx);
+                    M0[C0][j][0] = r.x;
+                    M0[C0][j][1] = r.y;
+                }
+            }
+            auto qcur = [&](int t) -> const R(&)[PY][PX] {   // level t's v[p]
+                if constexpr (L0C) return t == 0 ? M0[C0] : Q[F1][t];
+                else return Q[F1][t];
+            };
 
             // s_t = (x- + x+) + (y- + y+) of level t-1 at plane q-t, produced in
             // the previous step (ring slot pslot / level buffer prv; own and
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             auto xy_sums = [&](int t) {
                 const R* Pl = (t == 1) ? ring + pslot * RPLANE + HR * WX
                                        : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
-                const R(&v)[PY][PX] = Q[F1][t - 1];
+                const R(&v)[PY][PX] = qcur(t - 1);
                 V2 up, dn;
                 if constexpr (CL > 1) {
                     // level 0: the ring's halo rows; deeper: the neighbour slice's
@@ -590,14 +618,14 @@ __global__ void __launch_bounds__(32 * BY, MINB)
 
             mbar_wait(&full[slot], (gstep / RING_N) & 1);
             // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
-            R Nt[SLOTS == 2 ? D : 1][PY][PX];
+            R Nt[QS == 2 ? D : 1][PY][PX];
             auto newv = [&](int t) -> R(&)[PY][PX] {
-                if constexpr (SLOTS != 2) return Q[F2][t];
+                if constexpr (QS != 2) return Q[F2][t];
                 else return Nt[t];
             };
-            // SLOTS == 1: v[p-1] of level t-1, re-read from shared memory
-            R mv[SLOTS == 1 ? PY : 1][PX];
-            if constexpr (SLOTS == 1) {
+            // QS == 1: v[p-1] of level t-1, re-read from shared memory
+            R mv[QS == 1 ? PY : 1][PX];
+            if constexpr (QS == 1) {
                 const R* L2 = ring + pslot2 * RPLANE;   // level 0, plane q-2
 #pragma unroll
                 for (int j = 0; j < PY; ++j) {
@@ -621,10 +649,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             for (int t = 1; t <= D; ++t) {
                 if constexpr (P::DB) xy_sums(t);
                 const R(&mm)[PY][PX] = *([&]() -> const R(*)[PY][PX] {
-                    if constexpr (SLOTS == 1) return &mv;
+                    if constexpr (QS == 1) return &mv;
+                    else if constexpr (L0C) return t == 1 ? &M0[M0I] : &Q[F0][t - 1];
                     else return &Q[F0][t - 1];
                 }());
-                const R(&cc)[PY][PX] = Q[F1][t - 1];
+                const R(&cc)[PY][PX] = qcur(t - 1);
                 const R(&nn)[PY][PX] = newv(t - 1);
                 R(&dst)[PY][PX] = (t < D) ? newv(t < D ? t : 0) : out;
                 uint32_t inm = 0;   // SLOW: one bit per cell, in D_t this step
@@ -645,9 +674,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                         R upd = A::mul(A::add(s[t - 1][j][i], A::add(mm[j][i], nn[j][i])), sixth);
                         if constexpr (FAST) dst[j][i] = upd;
                         else dst[j][i] = ((inm >> (j * PX + i)) & 1u) ? upd : cc[j][i];
-                        if constexpr (SLOTS == 2) {   // shift level t-1's queue
-                            Q[0][t - 1][j][i] = cc[j][i];
-                            Q[1][t - 1][j][i] = nn[j][i];
+                        if constexpr (QS == 2) {   // shift level t-1's queue
+                            if (!L0C || t > 1) {
+                                Q[0][t - 1][j][i] = cc[j][i];
+                                Q[1][t - 1][j][i] = nn[j][i];
+                            }
                         }
                     }
                 if (SPLIT && t == 1 && gstep > 0) {
@@ -663,12 +694,12 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         // ring slot last read in step k-1: plane k-2 (k-3 with SLOTS == 1,
                         // which re-reads v[p-1] from slot k-2 at the start of a step)
-                        produce(SLOTS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
+                        produce(QS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
                     }
                 }
                 if (t < D) {
                     R* Pl = lvl + ((t - 1) * P::NBUF + cur) * PLANE;
-                    if constexpr (SLOTS == 1) {
+                    if constexpr (QS == 1) {
                         // this buffer still holds level t at plane q-t-1 = v[p-1]
                         // of level t+1: read it back, then store the full new plane
 #pragma unroll
@@ -746,7 +777,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
                 if (threadIdx.x == 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    produce(SLOTS == 1 ? pslot2 : pslot);
+                    produce(QS == 1 ? pslot2 : pslot);
                 }
             }
             ++gstep;
@@ -763,12 +794,12 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             else step(phase, std::false_type{}, st);
         };
 
-        if constexpr (SLOTS == 1) {
+        if constexpr (QS == 1 || L0C) {
             for (int st = 0; st < nsteps; st += 2) {
                 run(std::integral_constant<int, 0>{}, st);
                 if (st + 1 < nsteps) run(std::integral_constant<int, 1>{}, st + 1);
             }
-        } else if constexpr (SLOTS == 3) {
+        } else if constexpr (QS == 3) {
             for (int st = 0; st < nsteps; st += 3) {
                 run(std::integral_constant<int, 0>{}, st);
                 if (st + 1 < nsteps) run(std::integral_constant<int, 1>{}, st + 1);
