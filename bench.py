@@ -383,6 +383,7 @@ def main():
             "config": {"workload": desc, "T": T, "passes_per_step": len(passes),
                        "global_interior_zyx": list(gshape), "per_gpu_interior_zyx": list(shape),
                        "parallelism": f"zslab{world}", "variant": args.variant or "auto",
+                       "kernel": N.describe_variant(sp_dtype, T),
                        "halo_transport": transport if use_runner else None,
                        "l2": "inputs larger than L2 (one grid = %.1f GB >> 126 MB)" % (
                            grid.buffers[0].numel() * es / 1e9)},

@@ -185,6 +185,13 @@ int sp_set_tuning(int variant, int chunks);
  * Returns the previous values encoded as dynamic*1000 + strip. */
 int sp_set_schedule(int dynamic, int strip);
 
+/* Introspection (benchmarks, reports): the kernel variant a temporally blocked
+ * pass of depth T in dtype runs (after any sp_set_tuning override and the
+ * fallback for variants not built for T), and a one-line description of it
+ * (CTA shape, z-queue, CTAs per SM, step barrier, cluster form) in buf.
+ * Returns the variant index (>= 0) or a negative error code. */
+int sp_describe_variant(int dtype, int T, char* buf, int buflen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,7 @@ NVCC_FLAGS = [
 EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "sp_fill",
            "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_sweep_tb_part_peer", "sp_run_sweeps",
            "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule", "sp_ipc_export",
-           "sp_ipc_import", "sp_ipc_close", "sp_copy_in", "sp_copy_out")
+           "sp_ipc_import", "sp_ipc_close", "sp_copy_in", "sp_copy_out", "sp_describe_variant")
 
 
 class NativeUnavailable(RuntimeError):
@@ -126,6 +126,8 @@ def load_library():
     L.sp_digest.argtypes = [vp, ctypes.c_int, P(Layout), ctypes.c_int64, P(ctypes.c_uint64), vp]
     L.sp_probe_fp64.argtypes = [P(ctypes.c_double), P(ctypes.c_double)]
     L.sp_set_tuning.argtypes = [ctypes.c_int, ctypes.c_int]
+    if hasattr(L, "sp_describe_variant") or not override:
+        L.sp_describe_variant.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
     for name in EXPORTS:
         if override and not hasattr(L, name):
             continue   # older library under A/B comparison: tuning hooks may be absent
@@ -167,3 +169,12 @@ def i32x3(v):
 
 def launch_count() -> int:
     return int(load_library().sp_launch_count())
+
+
+def describe_variant(sp_dtype: int, T: int) -> str:
+    """One-line description of the K2 variant a depth-T pass runs (sp_describe_variant)."""
+    buf = ctypes.create_string_buffer(256)
+    v = load_library().sp_describe_variant(sp_dtype, T, buf, len(buf))   # host-only: no device needed
+    if v < 0:
+        check(-v)
+    return buf.value.decode()

@@ -699,6 +699,27 @@ int sp_set_schedule(int dynamic, int strip) {
     return prev;
 }
 
+int sp_describe_variant(int dtype, int T, char* buf, int buflen) {
+    if (elem_size(dtype) == 0) return -fail(SP_ERR_ARG, "unknown dtype %d", dtype);
+    if (T < 1 || T > 8) return -fail(SP_ERR_SCHEDULE, "temporal block depth T=%d outside 1..8", T);
+    const int v = variant_for(dtype, T);
+    const Variant& k = kVariants[v];
+    if (buf && buflen > 0) {
+        const char* q = k.slots == 1 ? "v[p-1] from shared memory"
+                      : k.slots == 2 ? "2-slot register z-queue"
+                      : k.slots == 3 ? "3-slot rotating register z-queue"
+                                     : "level 0 re-read from the ring, 2-slot queue above";
+        snprintf(buf, (size_t)buflen,
+                 "variant %d: %d warps x %d rows (64x%d footprint), %s, %d CTA/SM, %s step sync%s%s%s",
+                 v, k.by, k.py, k.by * k.py * k.cl, q, k.minb, k.split ? "split mbarrier" : "__syncthreads",
+                 k.rstore ? ", running output pointer" : "",
+                 k.ls > 1 ? (k.ls == 2 ? ", level split over a 2-CTA cluster" : ", level split over a 4-CTA cluster")
+                          : "",
+                 k.cl > 1 ? ", y-cooperative cluster" : "");
+    }
+    return v;
+}
+
 int sp_layout_make(int64_t nx, int64_t ny, int64_t nz, int64_t gx, int64_t gy, int64_t gz,
                    int dtype, sp_layout* out, int64_t* alloc_elems) {
     int es = elem_size(dtype);

@@ -177,3 +177,16 @@ def test_schedule_validation_matches_reference(sp):
         except sp.ScheduleError:
             ours_err = True
         assert ref_err == ours_err, ((nx, ny, nz), kw)
+
+
+def test_describe_variant_defaults(sp):
+    """The variant table's defaults (host-only introspection, no device needed)."""
+    N = sp._native
+    d = {(dt, T): N.describe_variant(dt, T) for dt in (N.SP_F64, N.SP_F32) for T in range(1, 9)}
+    assert "2 CTA/SM" in d[(N.SP_F64, 2)] and "8 warps x 4 rows" in d[(N.SP_F64, 2)]
+    assert "12 warps x 3 rows" in d[(N.SP_F64, 3)]
+    assert "level split over a 2-CTA cluster" in d[(N.SP_F64, 8)]
+    assert "level split" in d[(N.SP_F64, 6)]
+    assert "level split" not in d[(N.SP_F32, 8)]
+    with pytest.raises(ValueError):
+        N.describe_variant(N.SP_F64, 9)
