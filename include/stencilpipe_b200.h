@@ -185,6 +185,24 @@ int sp_set_tuning(int variant, int chunks);
  * Returns the previous values encoded as dynamic*1000 + strip. */
 int sp_set_schedule(int dynamic, int strip);
 
+/* Compressed single-array storage (R/grid.py:164-208; R/kernel.py:83-121):
+ * one temporally blocked pass of depth T IN PLACE over the box [lo, hi) of the
+ * allocation `buf` (layout L, walls on every face of the box).  Level-T plane
+ * p is stored at plane p - (2*chunk + T) (direction +1, z-chunks in ascending
+ * order) or p + (2*chunk + T) (direction -1, descending): no chunk overwrites
+ * a plane a chunk still reading it may need, which per-chunk counters in
+ * `counters` (device, >= ceil((hi-lo)/chunk) unsigned) enforce.  chunk >= 2T.
+ * The box's ghost shell does not move with it: sp_ghost_shell re-scatters it.
+ * Replaces update_region_compressed / _refresh_compressed_ghosts. */
+int sp_sweep_tb_inplace(void* buf, int dtype, const sp_layout* L, int T, const int64_t lo[3],
+                        const int64_t hi[3], int64_t chunk, int direction, void* counters,
+                        int64_t ncounters, void* stream);
+
+/* Ghost shell of a ghost-depth-1 box (layout L at `base`) packed into `shell`
+ * (sp_ghost_shell_elems elements): to_grid = 0 gathers, 1 scatters. */
+int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, void* stream);
+int64_t sp_ghost_shell_elems(int64_t nx, int64_t ny, int64_t nz);
+
 /* Introspection (benchmarks, reports): the kernel variant a temporally blocked
  * pass of depth T in dtype runs (after any sp_set_tuning override and the
  * fallback for variants not built for T), and a one-line description of it

@@ -6,8 +6,8 @@ sm_100a CUDA kernels behind the C ABI in include/stencilpipe_b200.h.
 Grids live in HBM; there is no CPU compute path.
 """
 
-from .grid import (ArrayPattern, FillPattern, GridDims, GridError, TwoGrid, allocate, dump_field,
-                   load_field)
+from .grid import (ArrayPattern, CompressedGrid, FillPattern, GridDims, GridError, TwoGrid, allocate,
+                   dump_field, load_field)
 from .kernel import (ONE_SIXTH, block_edges, stencil_point, sweep_naive,
                      sweep_spatial_blocked, update_block)
 from .pipeline import (DEFAULT_DEPTH, PipelineConfig, PipelineTimeout, ScheduleError,

@@ -36,7 +36,8 @@ NVCC_FLAGS = [
 EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "sp_fill",
            "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_sweep_tb_part_peer", "sp_run_sweeps",
            "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule", "sp_ipc_export",
-           "sp_ipc_import", "sp_ipc_close", "sp_copy_in", "sp_copy_out", "sp_describe_variant")
+           "sp_ipc_import", "sp_ipc_close", "sp_copy_in", "sp_copy_out", "sp_describe_variant",
+           "sp_sweep_tb_inplace", "sp_ghost_shell", "sp_ghost_shell_elems")
 
 
 class NativeUnavailable(RuntimeError):
@@ -126,6 +127,12 @@ def load_library():
     L.sp_digest.argtypes = [vp, ctypes.c_int, P(Layout), ctypes.c_int64, P(ctypes.c_uint64), vp]
     L.sp_probe_fp64.argtypes = [P(ctypes.c_double), P(ctypes.c_double)]
     L.sp_set_tuning.argtypes = [ctypes.c_int, ctypes.c_int]
+    if hasattr(L, "sp_sweep_tb_inplace") or not override:
+        L.sp_sweep_tb_inplace.argtypes = [vp, ctypes.c_int, P(Layout), ctypes.c_int, i64p, i64p,
+                                          ctypes.c_int64, ctypes.c_int, vp, ctypes.c_int64, vp]
+        L.sp_ghost_shell.argtypes = [vp, ctypes.c_int, P(Layout), vp, ctypes.c_int, vp]
+        L.sp_ghost_shell_elems.restype = ctypes.c_int64
+        L.sp_ghost_shell_elems.argtypes = [ctypes.c_int64] * 3
     if hasattr(L, "sp_describe_variant") or not override:
         L.sp_describe_variant.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
     for name in EXPORTS:

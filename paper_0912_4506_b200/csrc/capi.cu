@@ -443,10 +443,17 @@ struct PeerArgs {
     int64_t halo;      // planes [0, halo) go to lo, [nz - halo, nz) to hi
 };
 
+struct InPlace {
+    int64_t chunk;       // z-chunk length L (>= 2T)
+    int direction;       // +1: chunks ascending, planes stored 2L+T lower; -1: descending, higher
+    unsigned* counters;  // device, >= number of chunks; zeroed here on the stream
+    int64_t ncounters;
+};
+
 int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
                const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
                const int32_t ext_hi[3], const int64_t out_lo[3], const int64_t out_hi[3],
-               const PeerArgs* peer, void* stream);
+               const PeerArgs* peer, void* stream, const InPlace* inplace = nullptr);
 
 }  // namespace
 
@@ -780,6 +787,36 @@ int sp_sweep_tb_part_peer(const void* src, void* dst, int dtype, const sp_layout
     return sweep_part(src, dst, dtype, L, T, lo, hi, ext_lo, ext_hi, out_lo, out_hi, &p, stream);
 }
 
+int sp_sweep_tb_inplace(void* buf, int dtype, const sp_layout* L, int T, const int64_t lo[3],
+                        const int64_t hi[3], int64_t chunk, int direction, void* counters,
+                        int64_t ncounters, void* stream) {
+    if (direction != 1 && direction != -1) return fail(SP_ERR_ARG, "direction must be +1 or -1");
+    InPlace ip{chunk, direction, (unsigned*)counters, ncounters};
+    const int32_t zero[3] = {0, 0, 0};
+    return sweep_part(buf, buf, dtype, L, T, lo, hi, zero, zero, lo, hi, nullptr, stream, &ip);
+}
+
+int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, void* stream) {
+    int rc = check_layout(L, dtype);
+    if (rc) return rc;
+    if (!base || !shell) return fail(SP_ERR_ARG, "null argument");
+    if (L->gx != 1 || L->gy != 1 || L->gz != 1) return fail(SP_ERR_GRID, "ghost shell needs ghost depth 1");
+    sp::Shell g{L->nx, L->ny, L->nz, L->py, L->pz, L->origin, to_grid ? 1 : 0};
+    const int64_t rows = (L->nz + 2) * (L->ny + 2);
+    const int grid = (int)std::min<int64_t>(rows, 148 * 16);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == SP_F64) sp::ghost_shell_kernel<double><<<grid, 128, 0, s>>>((double*)base, (double*)shell, g);
+    else sp::ghost_shell_kernel<float><<<grid, 128, 0, s>>>((float*)base, (float*)shell, g);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "ghost_shell_kernel launch");
+    return SP_OK;
+}
+
+int64_t sp_ghost_shell_elems(int64_t nx, int64_t ny, int64_t nz) {
+    return 2 * (nx + 2) * (ny + 2) + nz * (2 * (nx + 2) + 2 * ny);
+}
+
 }  // extern "C"
 
 namespace {
@@ -787,11 +824,11 @@ namespace {
 int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
                const int64_t lo[3], const int64_t hi[3], const int32_t ext_lo[3],
                const int32_t ext_hi[3], const int64_t out_lo[3], const int64_t out_hi[3],
-               const PeerArgs* peer, void* stream) {
+               const PeerArgs* peer, void* stream, const InPlace* inplace) {
     int rc = check_layout(L, dtype);
     if (rc) return rc;
     if (!src || !dst || !lo || !hi || !out_lo || !out_hi) return fail(SP_ERR_ARG, "null argument");
-    if (src == dst) return fail(SP_ERR_ARG, "src and dst must be distinct arrays");
+    if (src == dst && !inplace) return fail(SP_ERR_ARG, "src and dst must be distinct arrays");
     if (T < 1 || T > 8) return fail(SP_ERR_SCHEDULE, "temporal block depth T=%d outside 1..8", T);
     const int64_t n[3] = {L->nz, L->ny, L->nx};
     const int64_t g[3] = {L->gz, L->gy, L->gx};
@@ -843,7 +880,9 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
         const int64_t nxo = out_hi[2] - out_lo[2];
         if ((nxo + ox_pair - 1) / ox_pair == (nxo + a.ox - 1) / a.ox) a.ox = ox_pair;
     }
-    const int variant = peer ? kPeerVariant : variant_for(dtype, T);
+    int variant = peer ? kPeerVariant : variant_for(dtype, T);
+    if (inplace && (kVariants[variant].cl > 1 || kVariants[variant].ls > 1))
+        variant = (dtype == SP_F64 ? usable_rt<double>(T, 12) : usable_rt<float>(T, 12)) ? 12 : 0;
     const int cl = kVariants[variant].cl;
     const int wy = kVariants[variant].by * kVariants[variant].py * cl;   // cluster footprint rows
     if (wy - 2 * T < 1) return fail(SP_ERR_SCHEDULE, "depth T=%d too deep for a %d-row footprint", T, wy);
@@ -876,15 +915,35 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     }
     if (g_chunks > 0) best_n = std::min<int64_t>(g_chunks, nzb);
     int64_t len = (nzb + best_n - 1) / best_n;
+    if (inplace) len = std::min<int64_t>(inplace->chunk, nzb);   // the in-place hazard rule fixes L
     int64_t nch = (nzb + len - 1) / len;
     if (tiles * nch >= (1ll << 31) - (1 << 20)) return fail(SP_ERR_SCHEDULE, "too many work units");
     a.chunk_len = (int)len;
     a.units = (int)(tiles * nch);
     a.strip = g_strip;
     a.sched = nullptr;
-    if (g_dynamic && cl == 1 && ls == 1) {
+    if ((g_dynamic || inplace) && cl == 1 && ls == 1) {   // in place: units must be claimed in order
         rc = sched_counter(&a.sched);
         if (rc) return rc;
+    }
+    a.zshift = 0;
+    a.reverse = 0;
+    a.nch = (int)nch;
+    a.cdone = nullptr;
+    if (inplace) {
+        // a chunk stores 2L+T planes away from where it reads, past the planes
+        // of the next chunk in order, so only chunks two and three back are
+        // still reading what it overwrites (TBArgs::cdone)
+        if (inplace->chunk < 2 * T) return fail(SP_ERR_SCHEDULE, "in-place chunk %lld < 2T", (long long)inplace->chunk);
+        const int64_t shift = 2 * len + T;
+        a.zshift = (int)(inplace->direction > 0 ? -shift : shift);
+        a.reverse = inplace->direction > 0 ? 0 : 1;
+        if (out_lo[0] + a.zshift < 0 || out_hi[0] + a.zshift > L->nz)
+            return fail(SP_ERR_GRID, "in-place pass stores outside the allocation (shift %d)", a.zshift);
+        if (!inplace->counters || inplace->ncounters < nch)
+            return fail(SP_ERR_ARG, "in-place pass needs %lld chunk counters", (long long)nch);
+        SP_CUDA(cudaMemsetAsync(inplace->counters, 0, (size_t)nch * sizeof(unsigned), (cudaStream_t)stream));
+        a.cdone = inplace->counters;
     }
     int grid = (int)std::min<int64_t>(a.units, slots);
     cudaStream_t s = (cudaStream_t)stream;

@@ -61,9 +61,34 @@ struct TBArgs {
     // NVLink -- and planes p >= rz_hi at (address + rd_hi) for the z+ one.
     int64_t rd_lo, rd_hi;      // element offsets from this grid to the neighbours' planes
     int rz_lo, rz_hi;
+    // In-place passes (compressed single-array storage; src == dst): level-T
+    // plane p is stored at plane p + zshift; chunks run in reverse order when
+    // `reverse`; cdone[c] counts the units of chunk c whose reads are complete,
+    // and a unit stores its first plane only once the chunks whose input
+    // planes it overwrites (c-2, c-3; c+2, c+3 in reverse) are complete.
+    int zshift, reverse, nch;
+    unsigned* cdone;           // null: not in place
 };
 
 // ---- small PTX helpers ------------------------------------------------------
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// In-place pass: wait until every unit of the chunks whose input planes the
+// current chunk overwrites has finished reading (see TBArgs::cdone).
+__device__ __forceinline__ void wait_chunks_read(const TBArgs& a, int c) {
+    const unsigned tiles = (unsigned)(a.ntx * a.nty);
+#pragma unroll
+    for (int k = 2; k <= 3; ++k) {
+        const int d = a.reverse ? c + k : c - k;
+        if (d >= 0 && d < a.nch)
+            while (ld_acquire_gpu(a.cdone + d) < tiles) __nanosleep(64);
+    }
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -233,7 +258,7 @@ template <> struct Arith<float> {
 
 // Unit decode: unit -> (tile x/y origin, z chunk).
 struct Unit {
-    int x0, y0, zc0, zc1;
+    int x0, y0, zc0, zc1, c;
 };
 
 // Units are z-chunk major; inside a chunk, tiles go y-major through column
@@ -255,7 +280,9 @@ __device__ __forceinline__ Unit decode_unit(const TBArgs& a, int u) {
         ty = r / a.ntx;
         tx = r - ty * a.ntx;
     }
+    if (a.reverse) c = a.nch - 1 - c;
     Unit w;
+    w.c = c;
     w.x0 = a.olo[2] + tx * a.ox;
     w.y0 = a.olo[1] + ty * a.oy;
     w.zc0 = a.olo[0] + c * a.chunk_len;
@@ -511,7 +538,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         }
         R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
         const int64_t pz = a.pz, py = a.py;
-        R* dnext = dcol + (int64_t)(w.zc0 - Te - D) * pz;   // plane q-D of step 0
+        R* dnext = dcol + (int64_t)(w.zc0 - Te - D + a.zshift) * pz;   // plane q-D of step 0
         // both x cells written and the pair 16-byte aligned (same for every row: py is)
         const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
         // every row of the patch is written with one 16-byte store (interior tiles)
@@ -617,6 +644,12 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             }
 
             mbar_wait(&full[slot], (gstep / RING_N) & 1);
+            if (a.cdone && st == nsteps - 1 && threadIdx.x == 0) {
+                // the unit's last plane has landed: all its global reads (TMA) are done
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                atomicAdd(a.cdone + w.c, 1u);
+            }
             // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
             R Nt[QS == 2 ? D : 1][PY][PX];
             auto newv = [&](int t) -> R(&)[PY][PX] {
@@ -734,7 +767,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     StAsync<R>::v2(base + (uint32_t)(j * WX * sizeof(R)), out[j][0], out[j][1], nx_full + 8u * s1);
                 ++gsent;
             } else if (st >= 2 * D) {
-                R* d = RSTORE ? dnext : dcol + (int64_t)(q - D) * pz;
+                if (a.cdone && st == 2 * D) {   // in place: first store of the unit
+                    if (lane == 0) wait_chunks_read(a, w.c);
+                    __syncwarp();
+                }
+                R* d = RSTORE ? dnext : dcol + (int64_t)(q - D + a.zshift) * pz;
                 auto put = [&](R* b) {
                     if (full_rows) {
 #pragma unroll
@@ -955,6 +992,43 @@ __global__ void __launch_bounds__(256) row_copy_kernel(const R* __restrict__ src
             const R v = __ldcs(s + x);
             __stcs(d + x, v);
             if (d2) __stcs(d2 + x, v);
+        }
+    }
+}
+
+// ---- K7: ghost shell gather / scatter (compressed storage) ---------------------
+//
+// The Dirichlet shell of a ghost-depth-1 box, packed: plane z = -1 and z = nz
+// whole ((ny+2)(nx+2) each), every interior plane as its frame (rows y = -1
+// and y = ny, then columns x = -1 and x = nx of rows 0..ny-1).  In-place
+// passes move the box by whole planes, so the shell is re-scattered at the
+// new position after each pass (R/kernel.py:83-102 refreshes it likewise).
+struct Shell {
+    int64_t nx, ny, nz, py, pz, origin;
+    int to_grid;   // 1: shell -> grid, 0: grid -> shell
+};
+
+template <typename R>
+__global__ void __launch_bounds__(128) ghost_shell_kernel(R* base, R* shell, const Shell g) {
+    const int64_t W = g.nx + 2, full = W * (g.ny + 2), frame = 2 * W + 2 * g.ny;
+    const int64_t rows = (g.nz + 2) * (g.ny + 2);
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t z = r / (g.ny + 2) - 1, y = r % (g.ny + 2) - 1;
+        R* row = base + g.origin + z * g.pz + y * g.py;
+        const bool zface = z < 0 || z >= g.nz;
+        const int64_t poff = z < 0 ? 0 : (z >= g.nz ? full + g.nz * frame : full + z * frame);
+        if (zface || y < 0 || y >= g.ny) {
+            // whole row x = -1 .. nx
+            R* sh = shell + poff + (zface ? (y + 1) * W : (y < 0 ? 0 : W));
+            for (int64_t x = threadIdx.x; x < W; x += blockDim.x) {
+                if (g.to_grid) row[x - 1] = sh[x];
+                else sh[x] = row[x - 1];
+            }
+        } else if (threadIdx.x < 2) {
+            const int64_t x = threadIdx.x == 0 ? -1 : g.nx;
+            R* sh = shell + poff + 2 * W + 2 * y + threadIdx.x;
+            if (g.to_grid) row[x] = *sh;
+            else *sh = row[x];
         }
     }
 }

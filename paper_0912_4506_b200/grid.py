@@ -323,6 +323,157 @@ class TwoGrid:
         return int(out.value)
 
 
+class CompressedGrid:
+    """Single-array storage in HBM (R/grid.py:164-208): one grid plus slack planes.
+
+    The reference shifts its box one cell diagonally per level and refreshes
+    the ghost faces before each block update (R/kernel.py:83-121).  On the
+    device every pass of depth T runs in place (``sp_sweep_tb_inplace``):
+    z-chunks of ``chunk`` planes go in order and store their level-T planes
+    2*chunk+T planes away from where they read them -- down when ascending,
+    up when descending -- so a chunk only overwrites planes that chunks two
+    and three back have finished reading (device counters enforce it).  The
+    box therefore moves by whole planes in z (``offset``); x/y stay put.  The
+    ghost shell is packed once (``sp_ghost_shell``) and re-scattered after
+    every pass.  HBM: (nz + 2 + slack) planes instead of 2 (nz + 2), with
+    slack = 4*chunk + 16 (any T <= 8, either direction from any offset).
+    """
+
+    storage = "compressed"
+
+    def __init__(self, dims: GridDims, pattern, slack: int | None = None, dtype=np.float64,
+                 device=None, chunk: int = 64):
+        import torch
+        if dims.ghost != 1:
+            raise GridError("compressed storage uses a one-layer ghost shell")
+        L = N.lib()
+        self.dims = dims
+        self.pattern = pattern
+        self.torch_dtype, self.sp_dtype = _torch_dtype(dtype)
+        self.dtype = np.float64 if self.sp_dtype == N.SP_F64 else np.float32
+        dev = torch.device("cuda") if device is None else torch.device(device)
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        self.chunk = max(16, min(int(chunk), dims.nz))     # >= 2T for every T <= 8
+        smax = 2 * self.chunk + 8
+        need = 2 * smax
+        if slack is not None and slack < 0:
+            raise GridError(f"slack must be >= 0, got {slack}")
+        self.slack = max(need, int(slack or 0))
+        lay = N.Layout()
+        n_alloc = ctypes.c_int64()
+        N.check(L.sp_layout_make(dims.nx, dims.ny, dims.nz + self.slack, 1, 1, 1, self.sp_dtype,
+                                 ctypes.byref(lay), ctypes.byref(n_alloc)))
+        self.blayout = lay                               # the whole allocation
+        self.layout = N.Layout(*lay.as_tuple())          # the box, relative to box_base()
+        self.layout.nz = dims.nz
+        self.offset = smax                               # box plane z sits at allocation plane z + offset
+        self._ascend_next = True
+        with torch.cuda.device(self.device):
+            self._buf = torch.zeros(n_alloc.value, dtype=self.torch_dtype, device=self.device)
+            nshell = L.sp_ghost_shell_elems(dims.nx, dims.ny, dims.nz)
+            self._shell = torch.empty(nshell, dtype=self.torch_dtype, device=self.device)
+            nch = -(-dims.nz // self.chunk)
+            self._counters = torch.zeros(nch, dtype=torch.int32, device=self.device)
+        self._fill(pattern)
+        with _on(self.device):
+            N.check(L.sp_ghost_shell(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
+                                     ctypes.c_void_p(self._shell.data_ptr()), 0, self.stream()))
+
+    # -- storage -------------------------------------------------------------
+
+    def stream(self):
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def _box_ptr(self):
+        """Base pointer under which ``layout`` describes the box at the current offset."""
+        es = self._buf.element_size()
+        return ctypes.c_void_p(self._buf.data_ptr() + self.offset * self.blayout.pz * es)
+
+    def _box_view(self):
+        lay, d = self.blayout, self.dims
+        off = lay.origin + (self.offset - 1) * lay.pz - lay.py - 1
+        return self._buf.as_strided((d.nz + 2, d.ny + 2, d.nx + 2), (lay.pz, lay.py, 1), off)
+
+    def _fill(self, pattern):
+        if isinstance(pattern, FillPattern):
+            with _on(self.device):
+                N.check(N.lib().sp_fill(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
+                                        ctypes.byref(pattern.to_c()), self.stream()))
+            return
+        if not hasattr(pattern, "evaluate"):
+            raise GridError(f"pattern {pattern!r} has no evaluate(lo, hi)")
+        import torch
+        d = self.dims
+        vals = np.asarray(pattern.evaluate((-1, -1, -1), (d.nz + 1, d.ny + 1, d.nx + 1)), dtype=self.dtype)
+        self._box_view().copy_(torch.from_numpy(np.ascontiguousarray(vals)))
+
+    @property
+    def buffers(self):
+        return (self._buf,)
+
+    @property
+    def current(self):
+        """The ghosted box (device view) at the current offset."""
+        return self._box_view()
+
+    # -- passes --------------------------------------------------------------
+
+    def run_passes(self, levels: int, depth: int) -> None:
+        """``levels`` levels as in-place passes of ``depth`` (stream-ordered)."""
+        d = self.dims
+        done = 0
+        while done < levels:
+            T = min(depth, levels - done)
+            s = 2 * min(self.chunk, d.nz) + T
+            up_ok = self.offset - s >= 0
+            down_ok = self.offset + s <= self.slack
+            ascend = up_ok if (self._ascend_next or not down_ok) else not down_ok
+            lo = (self.offset, 0, 0)
+            hi = (self.offset + d.nz, d.ny, d.nx)
+            with _on(self.device):
+                N.check(N.lib().sp_sweep_tb_inplace(
+                    ctypes.c_void_p(self._buf.data_ptr()), self.sp_dtype, ctypes.byref(self.blayout), int(T),
+                    N.i64x3(lo), N.i64x3(hi), int(self.chunk), 1 if ascend else -1,
+                    ctypes.c_void_p(self._counters.data_ptr()), self._counters.numel(), self.stream()))
+                self.offset += -s if ascend else s
+                N.check(N.lib().sp_ghost_shell(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
+                                               ctypes.c_void_p(self._shell.data_ptr()), 1, self.stream()))
+            self._ascend_next = not ascend
+            done += T
+
+    # -- host views ----------------------------------------------------------
+
+    def interior_device(self):
+        d = self.dims
+        return self._box_view()[1:1 + d.nz, 1:1 + d.ny, 1:1 + d.nx]
+
+    def interior(self) -> np.ndarray:
+        return self.interior_device().cpu().numpy()
+
+    def full_view(self) -> np.ndarray:
+        return self._box_view().cpu().numpy()
+
+    def value_at(self, i: int, j: int, k: int) -> float:
+        for idx, n in zip((i, j, k), (self.dims.nx, self.dims.ny, self.dims.nz)):
+            if not -1 <= idx < n + 1:
+                raise IndexError(f"index {(i, j, k)} outside interior+ghost range")
+        return float(self._box_view()[k + 1, j + 1, i + 1].item())
+
+    def digest(self, index_base: int = 0) -> int:
+        out = ctypes.c_uint64()
+        with _on(self.device):
+            N.check(N.lib().sp_digest(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
+                                      int(index_base), ctypes.byref(out), self.stream()))
+        return int(out.value)
+
+    @property
+    def hbm_bytes(self) -> int:
+        return self._buf.numel() * self._buf.element_size()
+
+
 class _on:
     """Make ``device`` current for the duration of a C-ABI call."""
 
@@ -376,10 +527,11 @@ def load_field(fh) -> tuple[GridDims, np.ndarray]:
 
 
 def allocate(dims: GridDims, mode: str, pattern, slack: int = 0, **kw):
-    """Allocate and initialise a device grid (R/grid.py:217-223); two-grid only."""
+    """Allocate and initialise a device grid (R/grid.py:217-223)."""
     if mode == "twogrid":
         return TwoGrid(dims, pattern, **kw)
     if mode == "compressed":
-        raise GridError("compressed storage is not implemented on the device "
-                        "(A/B ping-pong is the B200 layout; see DESIGN.md)")
+        if slack < 0:
+            raise GridError(f"slack must be >= 0, got {slack}")
+        return CompressedGrid(dims, pattern, slack=slack or None, **kw)
     raise GridError(f"unknown storage mode {mode!r}")

@@ -194,6 +194,9 @@ def sweeps(grid: TwoGrid, levels: int, depth: int | None = None) -> None:
     depth = depth or DEFAULT_DEPTH[grid.sp_dtype]
     if not 1 <= depth <= MAX_DEPTH:
         raise ScheduleError(f"device pass depth must be in 1..{MAX_DEPTH}")
+    if getattr(grid, "storage", None) == "compressed":
+        grid.run_passes(int(levels), int(depth))
+        return
     a, b = grid.buffers
     act = ctypes.c_int(grid.active)
     with _on(grid.device):
@@ -212,13 +215,16 @@ def run_node_sweeps(grid: TwoGrid, cfg: PipelineConfig, sweeps_: int,
     runs every sweep as ceil(U / depth) K2 passes.  The grid ends
     sweeps_*U levels ahead; ``current`` holds it.
     """
-    if not isinstance(grid, TwoGrid):
+    compressed = getattr(grid, "storage", None) == "compressed"
+    if cfg.storage != grid.storage:   # R/pipeline.py:301-316 checks the same pairing
+        raise ValueError(f"config expects {cfg.storage} storage but the device grid is {grid.storage}")
+    if not compressed and not isinstance(grid, TwoGrid):
         raise ValueError("config expects two-grid storage")
-    if cfg.storage != "twogrid":
-        raise ValueError("config expects compressed storage but the device grid is two-grid")
     U = cfg.levels_per_sweep
     check_schedule(grid.dims, cfg, level_domains)
     depth = cfg.depth or DEFAULT_DEPTH[grid.sp_dtype]
+    if compressed and level_domains is not None:
+        raise ScheduleError("compressed storage runs full-box node sweeps only (no level domains)")
     if level_domains is None:
         for _ in range(sweeps_):
             sweeps(grid, U, depth)
