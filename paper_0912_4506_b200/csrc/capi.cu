@@ -290,7 +290,7 @@ int variant_for(int dtype, int T) {
     return ok ? v : 0;
 }
 
-template <typename R, int T, int V, bool PEER = false>
+template <typename R, int T, int V, bool PEER = false, bool INPL = false>
 int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
                 cudaStream_t stream) {
     if constexpr (!usable<R, T, V>()) {
@@ -299,7 +299,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         constexpr Variant v = kVariants[V];
         using Pl = sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>;
         auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER, v.cl,
-                                  v.ls>;
+                                  v.ls, INPL>;
         const size_t smem = Pl::SMEM;
         // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
         static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
@@ -433,6 +433,42 @@ int launch_tb_peer(int T, const void* src, const sp_layout* L, const sp::TBArgs&
         case 8: return launch_tb_t<R, 8, kPeerVariant, true>(src, L, a, grid, s);
         default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
     }
+}
+
+// In-place passes (compressed storage) are separate instantiations with the
+// in-place hooks (keeping their registers out of the two-grid kernels).  The
+// per-unit chunk wait costs registers, so they use shapes with headroom: the
+// two-grid defaults that sit at the register cap (fp64 T=2 at two CTAs/SM,
+// T=3 12x3, T=4 8x4/3, fp32 T=2) would spill.
+template <typename R, int T>
+constexpr int inplace_variant() {
+    if constexpr (sizeof(R) == 8) {
+        return T == 1 ? 5 : T == 2 ? 1 : 12;
+    } else {
+        return T == 1 ? 14 : T == 2 ? 4 : T == 3 ? 22 : T == 4 ? 8 : T <= 6 ? 11 : 2;
+    }
+}
+
+template <typename R>
+int launch_tb_inplace(int T, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
+                      cudaStream_t s) {
+    switch (T) {
+        case 1: return launch_tb_t<R, 1, inplace_variant<R, 1>(), false, true>(src, L, a, grid, s);
+        case 2: return launch_tb_t<R, 2, inplace_variant<R, 2>(), false, true>(src, L, a, grid, s);
+        case 3: return launch_tb_t<R, 3, inplace_variant<R, 3>(), false, true>(src, L, a, grid, s);
+        case 4: return launch_tb_t<R, 4, inplace_variant<R, 4>(), false, true>(src, L, a, grid, s);
+        case 5: return launch_tb_t<R, 5, inplace_variant<R, 5>(), false, true>(src, L, a, grid, s);
+        case 6: return launch_tb_t<R, 6, inplace_variant<R, 6>(), false, true>(src, L, a, grid, s);
+        case 7: return launch_tb_t<R, 7, inplace_variant<R, 7>(), false, true>(src, L, a, grid, s);
+        case 8: return launch_tb_t<R, 8, inplace_variant<R, 8>(), false, true>(src, L, a, grid, s);
+        default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
+    }
+}
+
+int inplace_variant_rt(int dtype, int T) {
+    static const int f64[9] = {0, 5, 1, 12, 12, 12, 12, 12, 12};
+    static const int f32[9] = {0, 14, 4, 22, 8, 11, 11, 2, 2};
+    return (dtype == SP_F64 ? f64 : f32)[T];
 }
 
 struct PeerArgs {
@@ -796,17 +832,19 @@ int sp_sweep_tb_inplace(void* buf, int dtype, const sp_layout* L, int T, const i
     return sweep_part(buf, buf, dtype, L, T, lo, hi, zero, zero, lo, hi, nullptr, stream, &ip);
 }
 
+int64_t sp_ghost_shell_elems(int64_t nx, int64_t ny, int64_t nz);
+
 int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, void* stream) {
     int rc = check_layout(L, dtype);
     if (rc) return rc;
     if (!base || !shell) return fail(SP_ERR_ARG, "null argument");
     if (L->gx != 1 || L->gy != 1 || L->gz != 1) return fail(SP_ERR_GRID, "ghost shell needs ghost depth 1");
     sp::Shell g{L->nx, L->ny, L->nz, L->py, L->pz, L->origin, to_grid ? 1 : 0};
-    const int64_t rows = (L->nz + 2) * (L->ny + 2);
-    const int grid = (int)std::min<int64_t>(rows, 148 * 16);
+    const int64_t total = sp_ghost_shell_elems(L->nx, L->ny, L->nz);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
     cudaStream_t s = (cudaStream_t)stream;
-    if (dtype == SP_F64) sp::ghost_shell_kernel<double><<<grid, 128, 0, s>>>((double*)base, (double*)shell, g);
-    else sp::ghost_shell_kernel<float><<<grid, 128, 0, s>>>((float*)base, (float*)shell, g);
+    if (dtype == SP_F64) sp::ghost_shell_kernel<double><<<grid, 256, 0, s>>>((double*)base, (double*)shell, g);
+    else sp::ghost_shell_kernel<float><<<grid, 256, 0, s>>>((float*)base, (float*)shell, g);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "ghost_shell_kernel launch");
@@ -880,9 +918,7 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
         const int64_t nxo = out_hi[2] - out_lo[2];
         if ((nxo + ox_pair - 1) / ox_pair == (nxo + a.ox - 1) / a.ox) a.ox = ox_pair;
     }
-    int variant = peer ? kPeerVariant : variant_for(dtype, T);
-    if (inplace && (kVariants[variant].cl > 1 || kVariants[variant].ls > 1))
-        variant = (dtype == SP_F64 ? usable_rt<double>(T, 12) : usable_rt<float>(T, 12)) ? 12 : 0;
+    const int variant = peer ? kPeerVariant : (inplace ? inplace_variant_rt(dtype, T) : variant_for(dtype, T));
     const int cl = kVariants[variant].cl;
     const int wy = kVariants[variant].by * kVariants[variant].py * cl;   // cluster footprint rows
     if (wy - 2 * T < 1) return fail(SP_ERR_SCHEDULE, "depth T=%d too deep for a %d-row footprint", T, wy);
@@ -972,6 +1008,10 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
         }
         if (dtype == SP_F64) return launch_tb_peer<double>(T, src, L, a, grid, s);
         return launch_tb_peer<float>(T, src, L, a, grid, s);
+    }
+    if (inplace) {
+        if (dtype == SP_F64) return launch_tb_inplace<double>(T, src, L, a, grid, s);
+        return launch_tb_inplace<float>(T, src, L, a, grid, s);
     }
     if (dtype == SP_F64) return launch_tb<double>(T, variant, src, L, a, grid, s);
     return launch_tb<float>(T, variant, src, L, a, grid, s);

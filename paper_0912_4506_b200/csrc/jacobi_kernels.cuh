@@ -265,6 +265,7 @@ struct Unit {
 // strips `strip` tiles wide, so consecutive units are x/y neighbours (their
 // footprints share halo rows) -- under the dynamic schedule they are in
 // flight together and the shared rows come from L2.
+template <bool INPL = false>
 __device__ __forceinline__ Unit decode_unit(const TBArgs& a, int u) {
     int per = a.ntx * a.nty;
     int c = u / per;
@@ -280,7 +281,9 @@ __device__ __forceinline__ Unit decode_unit(const TBArgs& a, int u) {
         ty = r / a.ntx;
         tx = r - ty * a.ntx;
     }
-    if (a.reverse) c = a.nch - 1 - c;
+    if constexpr (INPL) {
+        if (a.reverse) c = a.nch - 1 - c;
+    }
     Unit w;
     w.c = c;
     w.x0 = a.olo[2] + tx * a.ox;
@@ -357,7 +360,7 @@ struct Plan {
 // CTA keeps only D levels of z-queue in registers, so T=8 fits where one CTA
 // holding all eight levels spills.
 template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV,
-          bool PEER = false, int CL = 1, int LS = 1>
+          bool PEER = false, int CL = 1, int LS = 1, bool INPL = false>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     // SLOTS = 4: levels >= 1 as SLOTS = 2; level 0's v[p] is re-read from the
@@ -367,6 +370,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     constexpr bool L0C = SLOTS == 4;
     constexpr int QS = L0C ? 2 : SLOTS;
     static_assert(SLOTS >= 1 && SLOTS <= 4, "z-queue slots");
+    static_assert(!INPL || (CL == 1 && LS == 1 && !PEER), "in-place passes: single-CTA variants");
     static_assert(LS == 1 || (T % LS == 0 && CL == 1 && !PEER && QS != 1),
                   "level split: depth a multiple of the cluster size");
     constexpr int D = T / LS;                    // levels this CTA applies
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         }
         uid[pseq++ & (P::NUID - 1)] = pu < a.units ? pu : -1;
         if (pu >= a.units) return;
-        const Unit pw = decode_unit(a, pu);
+        const Unit pw = decode_unit<INPL>(a, pu);
         pc0 = footprint_x<R>(a, pw.x0, T) + a.x_off;
         pc1 = pw.y0 - T + crank * WY - HR + a.gy;
         pc2 = pw.zc0 - Te + a.gz;
@@ -491,7 +495,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         mbar_wait(&full[gstep % RING_N], (gstep / RING_N) & 1);
         const int u = uid[cseq & (P::NUID - 1)];
         if (u < 0) break;
-        const Unit w = decode_unit(a, u);
+        const Unit w = decode_unit<INPL>(a, u);
         const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T + crank * WY;
         const int nsteps = (w.zc1 - w.zc0) + 2 * Te;
 
@@ -538,7 +542,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         }
         R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
         const int64_t pz = a.pz, py = a.py;
-        R* dnext = dcol + (int64_t)(w.zc0 - Te - D + a.zshift) * pz;   // plane q-D of step 0
+        // INPL: level-T plane p goes to plane p + zshift (compressed storage)
+        const int zsh = INPL ? a.zshift : 0;
+        R* dnext = dcol + (int64_t)(w.zc0 - Te - D + zsh) * pz;   // plane q-D of step 0
         // both x cells written and the pair 16-byte aligned (same for every row: py is)
         const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
         // every row of the patch is written with one 16-byte store (interior tiles)
@@ -644,12 +650,6 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             }
 
             mbar_wait(&full[slot], (gstep / RING_N) & 1);
-            if (a.cdone && st == nsteps - 1 && threadIdx.x == 0) {
-                // the unit's last plane has landed: all its global reads (TMA) are done
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                __threadfence();
-                atomicAdd(a.cdone + w.c, 1u);
-            }
             // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
             R Nt[QS == 2 ? D : 1][PY][PX];
             auto newv = [&](int t) -> R(&)[PY][PX] {
@@ -767,11 +767,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     StAsync<R>::v2(base + (uint32_t)(j * WX * sizeof(R)), out[j][0], out[j][1], nx_full + 8u * s1);
                 ++gsent;
             } else if (st >= 2 * D) {
-                if (a.cdone && st == 2 * D) {   // in place: first store of the unit
-                    if (lane == 0) wait_chunks_read(a, w.c);
-                    __syncwarp();
-                }
-                R* d = RSTORE ? dnext : dcol + (int64_t)(q - D + a.zshift) * pz;
+                R* d = RSTORE ? dnext : dcol + (int64_t)(q - D + zsh) * pz;
                 auto put = [&](R* b) {
                     if (full_rows) {
 #pragma unroll
@@ -831,6 +827,10 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             else step(phase, std::false_type{}, st);
         };
 
+        if constexpr (INPL) {   // stores of this unit overwrite planes chunks c-2, c-3 read
+            if (lane == 0) wait_chunks_read(a, w.c);
+            __syncwarp();
+        }
         if constexpr (QS == 1 || L0C) {
             for (int st = 0; st < nsteps; st += 2) {
                 run(std::integral_constant<int, 0>{}, st);
@@ -844,6 +844,14 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             }
         } else {
             for (int st = 0; st < nsteps; ++st) run(std::integral_constant<int, 0>{}, st);
+        }
+        if constexpr (INPL) {
+            if (threadIdx.x == 0) {
+                // this thread consumed the unit's last plane: all its global reads (TMA) are done
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                atomicAdd(a.cdone + w.c, 1u);
+            }
         }
     }
     // no CTA leaves while a neighbour may still read its planes or arrive on its barriers
@@ -1009,27 +1017,29 @@ struct Shell {
 };
 
 template <typename R>
-__global__ void __launch_bounds__(128) ghost_shell_kernel(R* base, R* shell, const Shell g) {
+__global__ void __launch_bounds__(256) ghost_shell_kernel(R* base, R* shell, const Shell g) {
+    // one thread per shell element, grid-stride; the packed order keeps the
+    // whole-row parts coalesced on both sides
     const int64_t W = g.nx + 2, full = W * (g.ny + 2), frame = 2 * W + 2 * g.ny;
-    const int64_t rows = (g.nz + 2) * (g.ny + 2);
-    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-        const int64_t z = r / (g.ny + 2) - 1, y = r % (g.ny + 2) - 1;
-        R* row = base + g.origin + z * g.pz + y * g.py;
-        const bool zface = z < 0 || z >= g.nz;
-        const int64_t poff = z < 0 ? 0 : (z >= g.nz ? full + g.nz * frame : full + z * frame);
-        if (zface || y < 0 || y >= g.ny) {
-            // whole row x = -1 .. nx
-            R* sh = shell + poff + (zface ? (y + 1) * W : (y < 0 ? 0 : W));
-            for (int64_t x = threadIdx.x; x < W; x += blockDim.x) {
-                if (g.to_grid) row[x - 1] = sh[x];
-                else sh[x] = row[x - 1];
-            }
-        } else if (threadIdx.x < 2) {
-            const int64_t x = threadIdx.x == 0 ? -1 : g.nx;
-            R* sh = shell + poff + 2 * W + 2 * y + threadIdx.x;
-            if (g.to_grid) row[x] = *sh;
-            else *sh = row[x];
+    const int64_t total = 2 * full + g.nz * frame;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t z, y, x;
+        if (i < full) {                                   // plane z = -1
+            z = -1; y = i / W - 1; x = i % W - 1;
+        } else if (i >= full + g.nz * frame) {            // plane z = nz
+            const int64_t k = i - full - g.nz * frame;
+            z = g.nz; y = k / W - 1; x = k % W - 1;
+        } else {
+            const int64_t k = i - full;
+            z = k / frame;
+            const int64_t f = k - z * frame;
+            if (f < 2 * W) { y = f < W ? -1 : g.ny; x = (f < W ? f : f - W) - 1; }
+            else { y = (f - 2 * W) >> 1; x = ((f - 2 * W) & 1) ? g.nx : -1; }
         }
+        R* cell = base + g.origin + z * g.pz + y * g.py + x;
+        if (g.to_grid) *cell = shell[i];
+        else shell[i] = *cell;
     }
 }
 

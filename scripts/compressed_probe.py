@@ -43,6 +43,13 @@ def main():
         sp.sweeps(c, depth, depth=depth)                       # warm-up
         tc = timed(lambda: sp.sweeps(c, levels, depth=depth))
         dc = c.digest()
+        import ctypes
+        from paper_0912_4506_b200 import _native as N
+        def scat():
+            for _ in range(10):
+                N.check(N.lib().sp_ghost_shell(c._box_ptr(), c.sp_dtype, ctypes.byref(c.layout),
+                                               ctypes.c_void_p(c._shell.data_ptr()), 1, c.stream()))
+        t_sc = timed(scat) / 10
         hb = c.hbm_bytes
         del c
         torch.cuda.empty_cache()
@@ -56,7 +63,7 @@ def main():
         out[depth] = {"compressed_glups": round(n ** 3 * levels / tc / 1e9, 1),
                       "twogrid_glups": round(n ** 3 * levels / tg / 1e9, 1),
                       "compressed_GB": round(hb / 1e9, 2), "twogrid_GB": round(hg / 1e9, 2),
-                      "same_digest": dc == dg}
+                      "same_digest": dc == dg, "ghost_scatter_ms": round(t_sc * 1e3, 3)}
         print(depth, out[depth], flush=True)
     print(json.dumps(out))
 
