@@ -486,6 +486,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         for (int i = 0; i < RING_N - (QS == 1 ? 2 : 1); ++i) produce(i);
     }
 
+    if constexpr (INPL) {   // the first unit's dependencies (see the end of the unit loop)
+        if (threadIdx.x == 0 && pu < a.units) wait_chunks_read(a, decode_unit<INPL>(a, pu).c);
+    }
     const R sixth = A::sixth();
     uint32_t gstep = 0;
     uint32_t gsent = 0;   // LS > 1, not last: planes pushed to the next rank so far
@@ -827,10 +830,6 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             else step(phase, std::false_type{}, st);
         };
 
-        if constexpr (INPL) {   // stores of this unit overwrite planes chunks c-2, c-3 read
-            if (lane == 0) wait_chunks_read(a, w.c);
-            __syncwarp();
-        }
         if constexpr (QS == 1 || L0C) {
             for (int st = 0; st < nsteps; st += 2) {
                 run(std::integral_constant<int, 0>{}, st);
@@ -851,6 +850,11 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 __threadfence();
                 atomicAdd(a.cdone + w.c, 1u);
+                // the next unit (already claimed by this thread, the producer) stores over
+                // planes chunks c-2, c-3 read: wait for them here, outside the step loop.
+                // The other warps store only after the step barrier has seen this
+                // thread's arrivals (release/acquire chain), 2T steps into the unit.
+                if (pu < a.units) wait_chunks_read(a, decode_unit<INPL>(a, pu).c);
             }
         }
     }
