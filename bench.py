@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--variant", type=int, default=0, help="kernel variant override (dev)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg")
+    ap.add_argument("--storage", choices=("twogrid", "compressed"), default="twogrid",
+                    help="A/B grids or single-array in-place storage (N=1)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--transport", choices=("p2p", "nccl"), default="p2p",
                     help="N>1 halo exchange: p2p = boundary kernels store into the neighbours' "
@@ -257,7 +259,8 @@ def main():
     pass_events = []
 
     if not use_runner:
-        grid = sp.TwoGrid(sp.GridDims(nx, ny, nz), pat, dtype=dtype, device=dev)
+        Grid = sp.CompressedGrid if args.storage == "compressed" else sp.TwoGrid
+        grid = Grid(sp.GridDims(nx, ny, nz), pat, dtype=dtype, device=dev)
 
         def step(record=False):
             for t in passes:
@@ -383,10 +386,13 @@ def main():
             "config": {"workload": desc, "T": T, "passes_per_step": len(passes),
                        "global_interior_zyx": list(gshape), "per_gpu_interior_zyx": list(shape),
                        "parallelism": f"zslab{world}", "variant": args.variant or "auto",
-                       "kernel": N.describe_variant(sp_dtype, T),
+                       "kernel": N.describe_variant(sp_dtype, T) if args.storage == "twogrid"
+                       else "in-place variant (compressed storage, sp_sweep_tb_inplace)",
+                       "storage": args.storage,
                        "halo_transport": transport if use_runner else None,
                        "l2": "inputs larger than L2 (one grid = %.1f GB >> 126 MB)" % (
-                           grid.buffers[0].numel() * es / 1e9)},
+                           grid.buffers[0].numel() * es / 1e9),
+                       "hbm_grid_bytes": sum(b.numel() * b.element_size() for b in grid.buffers)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
                          "kernel": f"tb_kernel T={T}", "peak_source": hbm_src,
@@ -478,7 +484,7 @@ def measure_e2e(sp, torch, np, grid, dtype, passes, dev, stream, steps=3):
     host_in = torch.empty(grid.host_shape(), dtype=grid.torch_dtype, pin_memory=True)
     host_in.copy_(grid.current.cpu())            # the initial field (untimed)
     host_out = [torch.empty(d.shape, dtype=grid.torch_dtype, pin_memory=True) for _ in range(2)]
-    grids = [grid] + [sp.TwoGrid(d, sp.FillPattern.constant(0.0), dtype=dtype, device=dev)
+    grids = [grid] + [type(grid)(d, sp.FillPattern.constant(0.0), dtype=dtype, device=dev)
                       for _ in range(2)]
     s_up, s_comp, s_down = (torch.cuda.Stream(dev) for _ in range(3))
     ev = lambda: torch.cuda.Event()                                      # noqa: E731

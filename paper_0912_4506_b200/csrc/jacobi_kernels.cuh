@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     }
 
     if constexpr (INPL) {   // the first unit's dependencies (see the end of the unit loop)
-        if (threadIdx.x == 0 && pu < a.units) wait_chunks_read(a, decode_unit<INPL>(a, pu).c);
+        if (threadIdx.x == 0 && uid[0] >= 0) wait_chunks_read(a, decode_unit<INPL>(a, uid[0]).c);
     }
     const R sixth = A::sixth();
     uint32_t gstep = 0;
@@ -850,11 +850,13 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 __threadfence();
                 atomicAdd(a.cdone + w.c, 1u);
-                // the next unit (already claimed by this thread, the producer) stores over
-                // planes chunks c-2, c-3 read: wait for them here, outside the step loop.
-                // The other warps store only after the step barrier has seen this
-                // thread's arrivals (release/acquire chain), 2T steps into the unit.
-                if (pu < a.units) wait_chunks_read(a, decode_unit<INPL>(a, pu).c);
+                // the next unit stores over planes chunks c-2, c-3 read: wait for them
+                // here, outside the step loop.  This thread (the producer) published
+                // its id in uid[] when it issued this unit's last plane, and may have
+                // claimed further units since.  The other warps store only after the
+                // step barrier has seen this thread's arrivals (release/acquire chain).
+                const int nu = uid[(cseq + 1) & (P::NUID - 1)];
+                if (nu >= 0) wait_chunks_read(a, decode_unit<INPL>(a, nu).c);
             }
         }
     }

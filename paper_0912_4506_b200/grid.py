@@ -473,6 +473,39 @@ class CompressedGrid:
     def hbm_bytes(self) -> int:
         return self._buf.numel() * self._buf.element_size()
 
+    # -- host transfers (stream-ordered; same contract as TwoGrid) ---------------
+
+    def host_shape(self):
+        d = self.dims
+        return (d.nz + 2, d.ny + 2, d.nx + 2)
+
+    def upload(self, field, stream=None) -> None:
+        """Replace the box (ghosts included) with a host field of shape host_shape()."""
+        import torch
+        t = field if isinstance(field, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(field))
+        if tuple(t.shape) != self.host_shape() or t.dtype != self.torch_dtype:
+            raise GridError(f"upload needs a {self.torch_dtype} field of shape {self.host_shape()}")
+        st = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
+        with torch.cuda.stream(st):
+            self._box_view().copy_(t, non_blocking=True)
+            with _on(self.device):
+                N.check(N.lib().sp_ghost_shell(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
+                                               ctypes.c_void_p(self._shell.data_ptr()), 0,
+                                               ctypes.c_void_p(st.cuda_stream)))
+
+    def download(self, out=None, stream=None):
+        """The interior into host memory (pass a pinned ``out`` for an asynchronous copy)."""
+        import torch
+        fresh = out is None
+        if fresh:
+            out = torch.empty(self.dims.shape, dtype=self.torch_dtype, pin_memory=True)
+        st = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
+        with torch.cuda.stream(st):
+            out.copy_(self.interior_device(), non_blocking=True)
+        if fresh:
+            torch.cuda.synchronize(self.device)
+        return out
+
 
 class _on:
     """Make ``device`` current for the duration of a C-ABI call."""

@@ -31,6 +31,7 @@ def _oracle(O, shape, kind, seed, faces, levels, dtype=np.float64):
     ((100, 12, 40), 16, 8, 16),     # deepest pass, chunk = 2T
     ((9, 7, 5), 7, 3, 32),          # one chunk shorter than the shift
     ((64, 64, 64), 10, 1, 16),      # single-level passes, alternating direction
+    ((50, 24, 40), 10, 2, 16),      # a 2-plane last chunk: the producer runs units ahead
 ])
 def test_compressed_matches_oracle(sp, O, dtype, shape, levels, depth, chunk):
     nz, ny, nx = shape
@@ -69,3 +70,18 @@ def test_compressed_footprint_and_errors(sp):
         sp.run_node_sweeps(g, cfg, 1)
     with pytest.raises(sp.GridError):
         sp.CompressedGrid(sp.GridDims(8, 8, 8, ghost=2), sp.FillPattern.constant(0.0))
+
+
+def test_compressed_upload_download_matches_twogrid(sp):
+    """The host-transfer API of the compressed grid (the bench's e2e path) against TwoGrid."""
+    import torch
+    d = sp.GridDims(40, 24, 50)
+    pat = sp.FillPattern.dirichlet_box("random", d.shape, FACES, seed=9)
+    src = sp.TwoGrid(d, pat)
+    field = torch.from_numpy(src.full_view()).pin_memory()
+    c = sp.CompressedGrid(d, sp.FillPattern.constant(0.0), chunk=16)
+    sp.sweeps(c, 3, depth=3)                 # move the box first: upload must land at the offset
+    c.upload(field)
+    sp.sweeps(c, 10, depth=2)
+    sp.sweeps(src, 10, depth=2)
+    assert _bitwise(c.download().numpy(), src.interior())
