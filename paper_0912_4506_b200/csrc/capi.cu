@@ -439,11 +439,13 @@ int launch_tb_peer(int T, const void* src, const sp_layout* L, const sp::TBArgs&
 // in-place hooks (keeping their registers out of the two-grid kernels).  The
 // per-unit chunk wait costs registers, so they use shapes with headroom: the
 // two-grid defaults that sit at the register cap (fp64 T=2 at two CTAs/SM,
-// T=3 12x3, T=4 8x4/3, fp32 T=2) would spill.
+// T=3 12x3, T=4 8x4/3, fp32 T=2) would spill.  fp64 T=2,3: 8x4/3 with one
+// __syncthreads per step (measured: 562 / 524-538 GLUP/s against 457 / 512
+// for 16x2/3 and 8x4/2 with the split barrier; at T=4 it spills: 355 vs 507).
 template <typename R, int T>
 constexpr int inplace_variant() {
     if constexpr (sizeof(R) == 8) {
-        return T == 1 ? 5 : T == 2 ? 1 : 12;
+        return T == 1 ? 5 : T <= 3 ? 13 : 12;
     } else {
         return T == 1 ? 14 : T == 2 ? 4 : T == 3 ? 22 : T == 4 ? 8 : T <= 6 ? 11 : 2;
     }
@@ -466,7 +468,7 @@ int launch_tb_inplace(int T, const void* src, const sp_layout* L, const sp::TBAr
 }
 
 int inplace_variant_rt(int dtype, int T) {
-    static const int f64[9] = {0, 5, 1, 12, 12, 12, 12, 12, 12};
+    static const int f64[9] = {0, 5, 13, 13, 12, 12, 12, 12, 12};
     static const int f32[9] = {0, 14, 4, 22, 8, 11, 11, 2, 2};
     return (dtype == SP_F64 ? f64 : f32)[T];
 }
