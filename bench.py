@@ -338,7 +338,8 @@ def main():
     hbm, hbm_src = measured_peaks()
     traffic = None
     tj = load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}
-    key = f"{args.workload}_T{T}_v{args.variant or 0}_n{world}"
+    key = f"{args.workload}_T{T}_v{args.variant or 0}_n{world}" + (
+        "_compressed" if args.storage == "compressed" else "")
     ncu_evidence = None
     if key in tj:
         traffic = tj[key].get("dram_bytes_per_launch")
