@@ -231,6 +231,8 @@ def main():
     dev = torch.device("cuda", local)
     dist = None
     use_runner = world > 1 or args.slab_runner
+    if use_runner and args.storage != "twogrid":
+        raise SystemExit("--storage compressed has no multi-GPU (slab runner) form")
     if use_runner:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
