@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_NAME = "libstencilpipe_b200.so"
 LIB_PATH = os.environ.get("SP_LIB_PATH") or os.path.join(_HERE, LIB_NAME)
-SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "jacobi_kernels.cuh")]
+SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "jacobi_kernels.cuh", "host.cuh", "tb_inst.cu")]
 HEADER = os.path.join(_ROOT, "include", "stencilpipe_b200.h")
 
 SP_OK, SP_ERR_GRID, SP_ERR_SCHEDULE, SP_ERR_DECOMP, SP_ERR_DEVICE, SP_ERR_ARG = range(6)
@@ -72,16 +72,45 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None,
         if os.path.exists("/usr/local/cuda/bin/nvcc"):
             nvcc = "/usr/local/cuda/bin/nvcc"
     tmp = target + ".tmp"
-    cmd = [nvcc, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", tmp,
-           os.path.join(_HERE, "csrc", "capi.cu")]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(os.path.dirname(target), "build", "obj" + ("_" + os.path.basename(target) if out else ""))
+    os.makedirs(objdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
+    cflags = [f for f in NVCC_FLAGS if f != "--shared"]
+    # one unit for the C ABI + small kernels, one per (dtype, T) for the K2
+    # instantiations (host.cuh / tb_inst.cu): compiled in parallel
+    jobs = [("capi", [os.path.join(_HERE, "csrc", "capi.cu")])]
+    for r in ("double", "float"):
+        for t in range(1, 9):
+            jobs.append((f"tb_{r}_{t}", [f"-DSP_INST_R={r}", f"-DSP_INST_T={t}",
+                                         os.path.join(_HERE, "csrc", "tb_inst.cu")]))
+
+    def compile_one(job):
+        name, args = job
+        obj = os.path.join(objdir, name + ".o")
+        r = subprocess.run([nvcc, *cflags, *dflags, "-c", "-o", obj, *args], capture_output=True, text=True)
+        return obj, r
+
+    from concurrent.futures import ThreadPoolExecutor
+    workers = max(1, min(len(jobs), (os.cpu_count() or 4)))
+    # the heaviest units first (deep fp64 / fp32 instantiations)
+    order = sorted(jobs, key=lambda j: (j[0] == "capi", -int(j[0][-1]) if j[0] != "capi" else 0))
+    with ThreadPoolExecutor(workers) as ex:
+        results = list(ex.map(compile_one, order))
+    log = []
+    for (obj, r), (name, _) in zip(results, order):
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed ({name}):\n{r.stderr}")
+        log.append(f"== {name}\n{r.stderr}")
+    res = subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "--shared", "-Xcompiler",
+                          "-fPIC", "-o", tmp, *[o for o, _ in results]],
+                         capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed:\n{res.stderr}")
+        raise RuntimeError(f"nvcc link failed:\n{res.stderr}")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write("".join(log))
     os.replace(tmp, target)
     with open(target + ".ptxas.log" if out else os.path.join(_HERE, "csrc", "ptxas.log"), "w") as fh:
-        fh.write(res.stderr)
+        fh.write("\n".join(log))
     return target
 
 

@@ -4,8 +4,7 @@
 // policy, TMA descriptor encoding, tile/z-chunk partitioning sized to the SM
 // count, argument validation and error reporting.  No grid memory is owned
 // here; the Python layer (PyTorch) allocates and passes raw pointers.
-#include "jacobi_kernels.cuh"
-#include "../../include/stencilpipe_b200.h"
+#include "host.cuh"
 
 #include <algorithm>
 #include <atomic>
@@ -18,18 +17,11 @@
 #include <string>
 #include <vector>
 
-#ifndef SP_L2_PROMO
-#define SP_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
-#endif
 
-namespace {
+namespace spi {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
-int g_chunks = 0;
-int g_use_k1 = 0;   // 1: single-level sweeps use the L1-streaming K1 kernel instead of K2(T=1)
-int g_dynamic = 1;  // K2 unit schedule: 1 = claimed in order from a device counter, 0 = round-robin
-int g_strip = 0;    // K2 unit order: tile-column strips this wide (0 = x-major rows)
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -45,16 +37,6 @@ int cuda_fail(cudaError_t e, const char* where) {
     return fail(SP_ERR_DEVICE, "%s: %s (%s)", where, cudaGetErrorString(e), cudaGetErrorName(e));
 }
 
-#define SP_CUDA(expr)                                   \
-    do {                                                \
-        cudaError_t _e = (expr);                        \
-        if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
-    } while (0)
-
-int elem_size(int dtype) { return dtype == SP_F64 ? 8 : (dtype == SP_F32 ? 4 : 0); }
-
-int64_t lo_x_mod(int64_t v, int64_t m) { return ((v % m) + m) % m; }
-
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -68,6 +50,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     });
     return fn;
 }
+
+}  // namespace spi
+
+namespace {
+
+using namespace spi;
+
+int g_chunks = 0;
+int g_use_k1 = 0;   // 1: single-level sweeps use the L1-streaming K1 kernel instead of K2(T=1)
+int g_dynamic = 1;  // K2 unit schedule: 1 = claimed in order from a device counter, 0 = round-robin
+int g_strip = 0;    // K2 unit order: tile-column strips this wide (0 = x-major rows)
+
 
 struct DevInfo {
     int sms = 0;
@@ -123,79 +117,8 @@ int sched_counter(unsigned** out) {
     return SP_OK;
 }
 
-// Kernel variants: CTA shape (warps BY x rows-per-thread PY; footprint is
-// 64 x BY*PY), z-queue depth (2 = shift by moves, 3 = rotating registers,
-// 1 = v[p-1] re-read from shared memory), CTAs per SM, TMA ring cap, running
-// output pointer, and the step synchronisation (split = per-warp mbarrier
-// arrive/wait on the level planes instead of one __syncthreads per step).
-struct Variant {
-    int by, py, slots, minb, ring;   // warps, rows/thread, z-queue slots, CTAs/SM, TMA ring cap
-    int rstore;                      // 1: running output pointer (see tb_kernel)
-    int split;                       // 1: split step barrier (see tb_kernel)
-    int zcap = 0;                    // > 0: z-chunks at most this many planes (L2 locality)
-    int cl = 1;                      // > 1: y-cooperative thread-block clusters of this size
-    int ls = 1;                      // 2: level-split pipeline over a cluster of two CTAs
-};
-constexpr Variant kVariants[] = {
-    {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
-    {16, 2, 3, 1, 8, 0, 1},  // 1: fp64 T=3
-    {8, 4, 2, 1, 8, 0, 0},   // 2: fp32 T>6
-    {8, 4, 3, 1, 8, 0, 1},   // 3
-    {8, 8, 2, 1, 8, 0, 0},   // 4: 64x64 footprint
-    {16, 2, 3, 1, 6, 0, 0},  // 5: fp64 T=1 (shallower ring streams better)
-    {16, 2, 1, 1, 8, 0, 1},  // 6: v[p-1] re-read from shared memory (16 warps), split
-    {8, 4, 1, 1, 8, 0, 1},   // 7: same, 8 warps
-    {8, 8, 2, 1, 8, 1, 0, 128},  // 8: fp32 T=3,4: 4 with the running output pointer
-    {8, 4, 2, 2, 8, 0, 1, 80},   // 9: fp64 T=2: two CTAs per SM (<= 128 registers), split
-    {8, 4, 1, 2, 8, 0, 1, 80},   // 10: two CTAs per SM, z-queue v[p-1] from shared memory, split
-    {16, 2, 2, 1, 8, 0, 1},  // 11: fp32 T=5,6: 0 with the split barrier
-    {8, 4, 2, 1, 8, 0, 1},   // 12: fp64 T>4: 2 with the split barrier
-    {8, 4, 3, 1, 8, 0, 0},   // 13: 3 with __syncthreads
-    {16, 2, 3, 1, 8, 0, 0},  // 14: fp32 T=1: 1 with __syncthreads
-    {8, 4, 3, 1, 8, 1, 1},   // 15: fp64 T=4: 3 with the running output pointer
-    {8, 8, 2, 2, 8, 1, 1, 128},  // 16: fp32 T=2: 8 at two CTAs per SM, split
-    // y-cooperative clusters (footprint 64 x cl*WY, edge rows over DSMEM)
-    {8, 4, 2, 2, 8, 0, 1, 0, 4},   // 17: 9 in clusters of 4
-    {16, 2, 3, 1, 8, 0, 1, 0, 4},  // 18: 1 in clusters of 4
-    {8, 4, 2, 2, 8, 1, 1, 80},     // 19: 9 with the running output pointer
-    // 12 warps x 3 rows (64x36 footprint): 3 warps per scheduler at <= 168 registers
-    {12, 3, 2, 1, 8, 1, 1},        // 20: fp64 T=4 alternative (ties 15)
-    {12, 3, 3, 1, 8, 1, 1},        // 21: fp64 T=3
-    {12, 6, 2, 1, 8, 1, 0, 128},   // 22: fp32 T=3 (64x72 footprint)
-    // level-split pipeline: two CTAs (two SMs) of a cluster apply levels 1..T/2 and T/2+1..T
-    {8, 4, 3, 1, 8, 1, 1, 0, 1, 2},    // 23: 15 per CTA (T=8: 4 levels each)
-    {8, 4, 2, 1, 8, 1, 1, 0, 1, 2},    // 24: 12 per CTA
-    {12, 3, 3, 1, 8, 1, 1, 0, 1, 2},   // 25: 21 per CTA
-    {8, 8, 2, 1, 8, 1, 1, 0, 1, 4},    // 26: 64x64 footprint, chain of four CTAs (T=8: 2 levels each)
-    // slots 4: level 0 re-read from the ring into step-parity registers (no level-0 moves)
-    {8, 4, 4, 1, 8, 0, 1},         // 27: fp64 T=5: 12 with slots 4
-};
-constexpr int kNumVariants = 28;
-static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
+
 int g_variant_override = -1;
-
-// Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
-// (16x2, 2 slots) fits every depth and is the fallback.
-template <typename R, int T, int V>
-constexpr bool compiled() {
-    if (V == 0) return true;
-    if (T == 1) return V == 5 || V == 14;
-    if (V == 17 || V == 18) return sizeof(R) == 8 && T >= 2 && T <= 4;
-    if (V == 19) return T == 2;
-    if (V == 20 || V == 21) return sizeof(R) == 8 && T >= 3 && T <= 4;
-    if (V == 22) return sizeof(R) == 4 && T >= 3 && T <= 4;
-    if (V >= 23 && V <= 25) return T == 4 || T == 6 || T == 8;
-    if (V == 26) return T == 8;
-    if (V == 27) return sizeof(R) == 8 && T >= 4 && T <= 5;
-
-    if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
-    if (V == 9 || V == 10) return T <= 4;
-    if (V == 16) return sizeof(R) == 4 && T == 2;   // deeper: spills at 128 registers
-    if (V == 11) return true;
-    if (V == 4) return T <= 4;
-    if (V == 2 || V == 12) return T >= 3;
-    return T <= 4;
-}
 
 // Default variant per (dtype, T), from same-box B200 sweeps
 // (profiles/r01_tuning.md, "split barrier" table).
@@ -220,18 +143,6 @@ int default_variant(int dtype, int T) {
         case 5:
         case 6: return 11;       // 16x2/2, split
         default: return 2;       // 8x4/2
-    }
-}
-
-template <typename R, int T, int V>
-constexpr bool usable() {
-    constexpr Variant v = kVariants[V];
-    if constexpr (!compiled<R, T, V>()) {
-        return false;
-    } else {
-        // level split: each CTA holds T/ls levels; the footprint still carries the T halo
-        return sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>::FITS &&
-               v.by * v.py * v.cl - 2 * T >= 1;
     }
 }
 
@@ -290,179 +201,18 @@ int variant_for(int dtype, int T) {
     return ok ? v : 0;
 }
 
-template <typename R, int T, int V, bool PEER = false, bool INPL = false>
-int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
-                cudaStream_t stream) {
-    if constexpr (!usable<R, T, V>()) {
-        return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
-    } else {
-        constexpr Variant v = kVariants[V];
-        using Pl = sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER, v.cl,
-                                  v.ls, INPL>;
-        const size_t smem = Pl::SMEM;
-        // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
-        static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
-        int dev = 0;
-        SP_CUDA(cudaGetDevice(&dev));
-        const uint64_t bit = 1ull << (dev & 63);
-        if (!(attr_set.load() & bit)) {
-            SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr_set.fetch_or(bit);
-        }
-        auto enc = encode_fn();
-        if (!enc) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
-        CUtensorMap map;
-        cuuint64_t gdim[3] = {(cuuint64_t)L->py, (cuuint64_t)(L->ny + 2 * L->gy),
-                              (cuuint64_t)(L->nz + 2 * L->gz)};
-        cuuint64_t gstride[2] = {(cuuint64_t)(L->py * sizeof(R)), (cuuint64_t)(L->pz * sizeof(R))};
-        cuuint32_t box[3] = {(cuuint32_t)sp::WX, (cuuint32_t)Pl::RROWS, 1};
-        cuuint32_t estr[3] = {1, 1, 1};
-        CUresult r = enc(&map, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-                         3, const_cast<void*>(src), gdim, gstride, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                         SP_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-        if constexpr (v.cl > 1 || v.ls > 1) {
-            constexpr int csize = v.cl > 1 ? v.cl : v.ls;
-            // persistent clusters: as many as can be co-resident, round-robin units
-            static std::atomic<uint64_t> occ[64] = {};   // per device: active clusters + 1
-            cudaLaunchConfig_t cfg = {};
-            cudaLaunchAttribute attr[1];
-            attr[0].id = cudaLaunchAttributeClusterDimension;
-            attr[0].val.clusterDim.x = csize;
-            attr[0].val.clusterDim.y = 1;
-            attr[0].val.clusterDim.z = 1;
-            cfg.blockDim = dim3(Pl::NT, 1, 1);
-            cfg.dynamicSmemBytes = smem;
-            cfg.stream = stream;
-            cfg.attrs = attr;
-            cfg.numAttrs = 1;
-            uint64_t nc = occ[dev & 63].load();
-            if (nc == 0) {
-                if (csize > 8) SP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-                int n = 0;
-                cfg.gridDim = dim3(csize * 148, 1, 1);
-                SP_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
-                if (n < 1) return fail(SP_ERR_DEVICE, "no cluster of %d CTAs fits (variant %d)", csize, V);
-                nc = (uint64_t)n + 1;
-                occ[dev & 63].store(nc);
-                if (getenv("SP_DEBUG_CLUSTER"))
-                    fprintf(stderr, "[sp] variant %d T=%d: %d active clusters of %d CTAs (smem %zu)\n", V, T, n,
-                            csize, smem);
-            }
-            const int clusters = (int)std::min<int64_t>(a.units, (int64_t)(nc - 1));
-            cfg.gridDim = dim3(clusters * csize, 1, 1);
-            SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a));
-        } else {
-            kern<<<grid, Pl::NT, smem, stream>>>(map, a);
-        }
-        g_launches.fetch_add(1, std::memory_order_relaxed);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "tb_kernel launch");
-        return SP_OK;
-    }
-}
-
-template <typename R, int T>
-int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
-                   cudaStream_t s) {
-    switch (v) {
-        case 0: return launch_tb_t<R, T, 0>(src, L, a, grid, s);
-        case 1: return launch_tb_t<R, T, 1>(src, L, a, grid, s);
-        case 2: return launch_tb_t<R, T, 2>(src, L, a, grid, s);
-        case 3: return launch_tb_t<R, T, 3>(src, L, a, grid, s);
-        case 4: return launch_tb_t<R, T, 4>(src, L, a, grid, s);
-        case 5: return launch_tb_t<R, T, 5>(src, L, a, grid, s);
-        case 6: return launch_tb_t<R, T, 6>(src, L, a, grid, s);
-        case 7: return launch_tb_t<R, T, 7>(src, L, a, grid, s);
-        case 8: return launch_tb_t<R, T, 8>(src, L, a, grid, s);
-        case 9: return launch_tb_t<R, T, 9>(src, L, a, grid, s);
-        case 10: return launch_tb_t<R, T, 10>(src, L, a, grid, s);
-        case 11: return launch_tb_t<R, T, 11>(src, L, a, grid, s);
-        case 12: return launch_tb_t<R, T, 12>(src, L, a, grid, s);
-        case 13: return launch_tb_t<R, T, 13>(src, L, a, grid, s);
-        case 14: return launch_tb_t<R, T, 14>(src, L, a, grid, s);
-        case 15: return launch_tb_t<R, T, 15>(src, L, a, grid, s);
-        case 16: return launch_tb_t<R, T, 16>(src, L, a, grid, s);
-        case 17: return launch_tb_t<R, T, 17>(src, L, a, grid, s);
-        case 18: return launch_tb_t<R, T, 18>(src, L, a, grid, s);
-        case 19: return launch_tb_t<R, T, 19>(src, L, a, grid, s);
-        case 20: return launch_tb_t<R, T, 20>(src, L, a, grid, s);
-        case 21: return launch_tb_t<R, T, 21>(src, L, a, grid, s);
-        case 22: return launch_tb_t<R, T, 22>(src, L, a, grid, s);
-        case 23: return launch_tb_t<R, T, 23>(src, L, a, grid, s);
-        case 24: return launch_tb_t<R, T, 24>(src, L, a, grid, s);
-        case 25: return launch_tb_t<R, T, 25>(src, L, a, grid, s);
-        case 26: return launch_tb_t<R, T, 26>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 27>(src, L, a, grid, s);
-    }
-}
-
 template <typename R>
-int launch_tb(int T, int v, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
-              cudaStream_t s) {
+int launch_tb_kind(int kind, int T, int v, const void* src, const sp_layout* L, const sp::TBArgs& a,
+                   int grid, cudaStream_t s) {
     switch (T) {
-        case 1: return launch_variant<R, 1>(v, src, L, a, grid, s);
-        case 2: return launch_variant<R, 2>(v, src, L, a, grid, s);
-        case 3: return launch_variant<R, 3>(v, src, L, a, grid, s);
-        case 4: return launch_variant<R, 4>(v, src, L, a, grid, s);
-        case 5: return launch_variant<R, 5>(v, src, L, a, grid, s);
-        case 6: return launch_variant<R, 6>(v, src, L, a, grid, s);
-        case 7: return launch_variant<R, 7>(v, src, L, a, grid, s);
-        case 8: return launch_variant<R, 8>(v, src, L, a, grid, s);
-        default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
-    }
-}
-
-// Peer-store launches (boundary slabs of a z-slab rank) use the fallback
-// variant 0 only: they cover h planes, a small share of a step.
-constexpr int kPeerVariant = 0;
-
-template <typename R>
-int launch_tb_peer(int T, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
-                   cudaStream_t s) {
-    switch (T) {
-        case 1: return launch_tb_t<R, 1, kPeerVariant, true>(src, L, a, grid, s);
-        case 2: return launch_tb_t<R, 2, kPeerVariant, true>(src, L, a, grid, s);
-        case 3: return launch_tb_t<R, 3, kPeerVariant, true>(src, L, a, grid, s);
-        case 4: return launch_tb_t<R, 4, kPeerVariant, true>(src, L, a, grid, s);
-        case 5: return launch_tb_t<R, 5, kPeerVariant, true>(src, L, a, grid, s);
-        case 6: return launch_tb_t<R, 6, kPeerVariant, true>(src, L, a, grid, s);
-        case 7: return launch_tb_t<R, 7, kPeerVariant, true>(src, L, a, grid, s);
-        case 8: return launch_tb_t<R, 8, kPeerVariant, true>(src, L, a, grid, s);
-        default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
-    }
-}
-
-// In-place passes (compressed storage) are separate instantiations with the
-// in-place hooks (keeping their registers out of the two-grid kernels).  The
-// per-unit chunk wait costs registers, so they use shapes with headroom: the
-// two-grid defaults that sit at the register cap (fp64 T=2 at two CTAs/SM,
-// T=3 12x3, T=4 8x4/3, fp32 T=2) would spill.  fp64 T=2,3: 8x4/3 with one
-// __syncthreads per step (measured: 562 / 524-538 GLUP/s against 457 / 512
-// for 16x2/3 and 8x4/2 with the split barrier; at T=4 it spills: 355 vs 507).
-template <typename R, int T>
-constexpr int inplace_variant() {
-    if constexpr (sizeof(R) == 8) {
-        return T == 1 ? 5 : T <= 3 ? 13 : 12;
-    } else {
-        return T == 1 ? 14 : T == 2 ? 4 : T == 3 ? 22 : T == 4 ? 8 : T <= 6 ? 11 : 2;
-    }
-}
-
-template <typename R>
-int launch_tb_inplace(int T, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
-                      cudaStream_t s) {
-    switch (T) {
-        case 1: return launch_tb_t<R, 1, inplace_variant<R, 1>(), false, true>(src, L, a, grid, s);
-        case 2: return launch_tb_t<R, 2, inplace_variant<R, 2>(), false, true>(src, L, a, grid, s);
-        case 3: return launch_tb_t<R, 3, inplace_variant<R, 3>(), false, true>(src, L, a, grid, s);
-        case 4: return launch_tb_t<R, 4, inplace_variant<R, 4>(), false, true>(src, L, a, grid, s);
-        case 5: return launch_tb_t<R, 5, inplace_variant<R, 5>(), false, true>(src, L, a, grid, s);
-        case 6: return launch_tb_t<R, 6, inplace_variant<R, 6>(), false, true>(src, L, a, grid, s);
-        case 7: return launch_tb_t<R, 7, inplace_variant<R, 7>(), false, true>(src, L, a, grid, s);
-        case 8: return launch_tb_t<R, 8, inplace_variant<R, 8>(), false, true>(src, L, a, grid, s);
+        case 1: return launch_kind<R, 1>(kind, v, src, L, a, grid, s);
+        case 2: return launch_kind<R, 2>(kind, v, src, L, a, grid, s);
+        case 3: return launch_kind<R, 3>(kind, v, src, L, a, grid, s);
+        case 4: return launch_kind<R, 4>(kind, v, src, L, a, grid, s);
+        case 5: return launch_kind<R, 5>(kind, v, src, L, a, grid, s);
+        case 6: return launch_kind<R, 6>(kind, v, src, L, a, grid, s);
+        case 7: return launch_kind<R, 7>(kind, v, src, L, a, grid, s);
+        case 8: return launch_kind<R, 8>(kind, v, src, L, a, grid, s);
         default: return fail(SP_ERR_ARG, "temporal block depth T=%d outside 1..8", T);
     }
 }
@@ -1008,15 +758,15 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
             a.rd_hi = delta(peer->hi, peer->hi_shift);
             a.rz_hi = (int)(L->nz - peer->halo);
         }
-        if (dtype == SP_F64) return launch_tb_peer<double>(T, src, L, a, grid, s);
-        return launch_tb_peer<float>(T, src, L, a, grid, s);
+        if (dtype == SP_F64) return launch_tb_kind<double>(1, T, 0, src, L, a, grid, s);
+        return launch_tb_kind<float>(1, T, 0, src, L, a, grid, s);
     }
     if (inplace) {
-        if (dtype == SP_F64) return launch_tb_inplace<double>(T, src, L, a, grid, s);
-        return launch_tb_inplace<float>(T, src, L, a, grid, s);
+        if (dtype == SP_F64) return launch_tb_kind<double>(2, T, 0, src, L, a, grid, s);
+        return launch_tb_kind<float>(2, T, 0, src, L, a, grid, s);
     }
-    if (dtype == SP_F64) return launch_tb<double>(T, variant, src, L, a, grid, s);
-    return launch_tb<float>(T, variant, src, L, a, grid, s);
+    if (dtype == SP_F64) return launch_tb_kind<double>(0, T, variant, src, L, a, grid, s);
+    return launch_tb_kind<float>(0, T, variant, src, L, a, grid, s);
 }
 
 }  // namespace

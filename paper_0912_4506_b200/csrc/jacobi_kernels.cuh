@@ -242,17 +242,53 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
 
 // ---- exact arithmetic -------------------------------------------------------
 
+// add2/mul2 apply the op to the two cells of an x pair: (r0, r1) = (a0 op b0,
+// a1 op b1).  fp32 issues one packed FADD2/FMUL2 (sm_100 `add.rn.f32x2`,
+// round-to-nearest per lane -- the same bits as two scalar ops), halving the
+// FP instruction count of the pair; fp64 has no packed form (two DADD/DMUL).
 template <typename R> struct Arith;
 template <> struct Arith<double> {
     using V2 = double2;
     __device__ static __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
     __device__ static __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+    __device__ static __forceinline__ void add2(double& r0, double& r1, double a0, double a1, double b0,
+                                                double b1) {
+        r0 = __dadd_rn(a0, b0);
+        r1 = __dadd_rn(a1, b1);
+    }
+    __device__ static __forceinline__ void mul2(double& r0, double& r1, double a0, double a1, double b) {
+        r0 = __dmul_rn(a0, b);
+        r1 = __dmul_rn(a1, b);
+    }
     __device__ static __forceinline__ double sixth() { return 1.0 / 6.0; }  // 0x3FC5555555555555
 };
 template <> struct Arith<float> {
     using V2 = float2;
     __device__ static __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
     __device__ static __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+#ifdef SP_SCALAR_F32   // A/B builds: two scalar FADD/FMUL per pair
+    __device__ static __forceinline__ void add2(float& r0, float& r1, float a0, float a1, float b0, float b1) {
+        r0 = __fadd_rn(a0, b0);
+        r1 = __fadd_rn(a1, b1);
+    }
+    __device__ static __forceinline__ void mul2(float& r0, float& r1, float a0, float a1, float b) {
+        r0 = __fmul_rn(a0, b);
+        r1 = __fmul_rn(a1, b);
+    }
+#else
+    __device__ static __forceinline__ void add2(float& r0, float& r1, float a0, float a1, float b0, float b1) {
+        asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+            "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+            : "=f"(r0), "=f"(r1)
+            : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+    }
+    __device__ static __forceinline__ void mul2(float& r0, float& r1, float a0, float a1, float b) {
+        asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %4};\n\t"
+            "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+            : "=f"(r0), "=f"(r1)
+            : "f"(a0), "f"(a1), "f"(b));
+    }
+#endif
     __device__ static __forceinline__ float sixth() { return (float)(1.0 / 6.0); }  // 0x3E2AAAAB
 };
 
@@ -400,6 +436,10 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     // arithmetic of step k overlap the slowest warps of step k-1; thread 0
     // refills the ring slot freed by step k-1 right after that wait.
     constexpr bool SPLIT = SPLITV && D >= 2 && P::DB;
+    // fp32: pair the cells of an x pair into packed FADD2/FMUL2 (measured: fp32
+    // T=4 +4 %); not at two CTAs per SM, where the pairing spills at 128
+    // registers (fp32 T=2 -5 %).  fp64: no packed form; the order is the same.
+    constexpr bool PACK = sizeof(R) == 4 && MINB == 1;
 
     const int lane = threadIdx.x & 31;
     const int wy = threadIdx.x >> 5;
@@ -642,8 +682,17 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     R ym1 = (j == 0) ? up.y : v[j > 0 ? j - 1 : 0][1];
                     R yp0 = (j == PY - 1) ? dn.x : v[j + 1 < PY ? j + 1 : j][0];
                     R yp1 = (j == PY - 1) ? dn.y : v[j + 1 < PY ? j + 1 : j][1];
-                    s[t - 1][j][0] = A::add(A::add(lft, v[j][1]), A::add(ym0, yp0));
-                    s[t - 1][j][1] = A::add(A::add(v[j][0], rgt), A::add(ym1, yp1));
+                    // ((x- + x+) + (y- + y+)): the x sums pair a lane neighbour's
+                    // cell with our own (scalar adds write them as a pair), the
+                    // y sums and the total are pair ops
+                    if constexpr (!PACK) {
+                        s[t - 1][j][0] = A::add(A::add(lft, v[j][1]), A::add(ym0, yp0));
+                        s[t - 1][j][1] = A::add(A::add(v[j][0], rgt), A::add(ym1, yp1));
+                    } else {
+                        R x0 = A::add(lft, v[j][1]), x1 = A::add(v[j][0], rgt), y0, y1;
+                        A::add2(y0, y1, ym0, ym1, yp0, yp1);
+                        A::add2(s[t - 1][j][0], s[t - 1][j][1], x0, x1, y0, y1);
+                    }
                 }
             };
             if constexpr (!P::DB) {
@@ -704,10 +753,21 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                         if (zin && ((yb >> j) & 1u)) inm |= xb << (j * PX);
                 }
 #pragma unroll
-                for (int j = 0; j < PY; ++j)
+                for (int j = 0; j < PY; ++j) {
+                    // (s + (z- + z+)) * ONE_SIXTH for the pair (PX == 2)
+                    R zs[PX], us[PX], ups[PX];
+                    if constexpr (!PACK) {
+#pragma unroll
+                        for (int i = 0; i < PX; ++i)
+                            ups[i] = A::mul(A::add(s[t - 1][j][i], A::add(mm[j][i], nn[j][i])), sixth);
+                    } else {
+                        A::add2(zs[0], zs[1], mm[j][0], mm[j][1], nn[j][0], nn[j][1]);
+                        A::add2(us[0], us[1], s[t - 1][j][0], s[t - 1][j][1], zs[0], zs[1]);
+                        A::mul2(ups[0], ups[1], us[0], us[1], sixth);
+                    }
 #pragma unroll
                     for (int i = 0; i < PX; ++i) {
-                        R upd = A::mul(A::add(s[t - 1][j][i], A::add(mm[j][i], nn[j][i])), sixth);
+                        const R upd = ups[i];
                         if constexpr (FAST) dst[j][i] = upd;
                         else dst[j][i] = ((inm >> (j * PX + i)) & 1u) ? upd : cc[j][i];
                         if constexpr (QS == 2) {   // shift level t-1's queue
@@ -717,6 +777,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                             }
                         }
                     }
+                }
                 if (SPLIT && t == 1 && gstep > 0) {
                     // step k-1 is complete in every warp: its reads of this
                     // buffer are done and its level planes are visible
@@ -943,7 +1004,7 @@ __device__ __forceinline__ double random_value(int64_t z, int64_t y, int64_t x, 
     return __dmul_rn((double)(h >> 11), 0x1.0p-53);
 }
 
-__device__ double pattern_value(const FillArgs& f, int64_t z, int64_t y, int64_t x) {
+__device__ inline double pattern_value(const FillArgs& f, int64_t z, int64_t y, int64_t x) {
     int64_t c0 = z + f.gorigin[0], c1 = y + f.gorigin[1], c2 = x + f.gorigin[2];
     if (f.has_faces) {
         if (c0 < 0) return f.faces[0];
@@ -1071,6 +1132,7 @@ __global__ void digest_kernel(const R* base, int64_t nx, int64_t ny, int64_t nz,
     if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)acc);
 }
 
+#ifndef SP_INST_UNIT   // defined once, in capi.cu
 // ---- FP64 add-throughput probe ------------------------------------------------
 
 __global__ void __launch_bounds__(256) fp64_probe_kernel(double seed, int iters, double* sink) {
@@ -1087,5 +1149,6 @@ __global__ void __launch_bounds__(256) fp64_probe_kernel(double seed, int iters,
     double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
     if (r == 12345.678) sink[threadIdx.x] = r;  // never true; keeps the chain alive
 }
+#endif
 
 }  // namespace sp
