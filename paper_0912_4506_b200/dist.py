@@ -50,6 +50,10 @@ class CudaEngine:
         from .decomp import local_grid
         return local_grid(decomp, rank, pattern, dtype=dtype, device=device)
 
+    def default_depth(self, grid):
+        """Tuned levels per pass for the grid's dtype (pipeline.DEFAULT_DEPTH)."""
+        return DEFAULT_DEPTH[grid.sp_dtype]
+
     def run_pass(self, grid, T, lo, hi, e_lo, e_hi, out_lo, out_hi):
         from .pipeline import run_pass
         run_pass(grid, T, lo, hi, e_lo, e_hi, out_lo=out_lo, out_hi=out_hi)
@@ -102,9 +106,6 @@ class PeerBuffer:
 
     def data_ptr(self) -> int:
         return self.ptr
-
-    def default_depth(self, grid):
-        return DEFAULT_DEPTH[grid.sp_dtype]
 
 
 class SlabRunner:

@@ -181,6 +181,13 @@ class TwoGrid:
 
     # -- storage -------------------------------------------------------------
 
+    def reset(self, pattern=None) -> None:
+        """Re-initialise both arrays from ``pattern`` (default: the construction
+        pattern) and make A current, as constructing the grid again would."""
+        self._fill(self.pattern if pattern is None else pattern)
+        self._b.copy_(self._a)
+        self.active = 0
+
     def stream(self):
         import torch
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)

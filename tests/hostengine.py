@@ -38,6 +38,12 @@ class HostGrid:
         fill = O.lib().or_fill_f64 if dtype == np.float64 else O.lib().or_fill_f32
         fill(self._a.data_ptr(), ctypes.byref(olay), ctypes.byref(O._c_pattern(pattern)))
         self._b.copy_(self._a)
+        self._init = self._a.clone()
+        self.active = 0
+
+    def reset(self):
+        self._a.copy_(self._init)
+        self._b.copy_(self._init)
         self.active = 0
 
     @property

@@ -110,7 +110,8 @@ def _e2e_worker(rank, world, port, q, transport="nccl"):
         base = O.BoxPattern("random", seed=0, faces=Z1, global_shape=gshape)
         r = SlabRunner(sp.GridDims(12, 10, 40), None, h=4, dtype=np.float64, depth=4,
                        engine=HostEngine(base), transport=transport)
-        e2e = bench.measure_e2e_dist(torch, dist, r, [4, 4], torch.device("cpu"), world, steps=2)
+        e2e = bench.measure_e2e_dist(torch, dist, [r], [4, 4], torch.device("cpu"), world, 40 * 10 * 12,
+                                     steps=2)
         full = r.gather()
         if rank == 0:
             q.put((full, e2e, r.grid.current.numel()))

@@ -97,3 +97,40 @@ def test_p2p_runner_two_processes_one_gpu(O, world, h, levels):
         assert p.exitcode == 0
     assert msgs > 0
     assert _bitwise(full, _oracle(O, (48, 20, 70), FACES, sum(levels)))
+
+
+def _default_depth_worker(port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+    import paper_0912_4506_b200 as sp
+    from paper_0912_4506_b200.dist import SlabRunner
+    from paper_0912_4506_b200.pipeline import DEFAULT_DEPTH
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        shape = (30, 20, 70)
+        pat = sp.FillPattern.dirichlet_box("random", shape, FACES, seed=0)
+        # depth=None: the engine's tuned default (CudaEngine.default_depth)
+        r = SlabRunner(sp.GridDims(70, 20, 30), pat, h=4, dtype=np.float64, device=torch.device("cuda", 0))
+        assert r.depth == DEFAULT_DEPTH[sp._native.SP_F64]
+        for lv in (4, 4, 2):
+            r.step(levels=lv)
+        r.finish()
+        q.put(r.gather())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_runner_default_depth(O):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_default_depth_worker, args=(_free_port(), q))
+    p.start()
+    full = q.get(timeout=300)
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    assert _bitwise(full, _oracle(O, (30, 20, 70), FACES, 10))

@@ -190,3 +190,16 @@ def test_describe_variant_defaults(sp):
     assert "level split" not in d[(N.SP_F32, 8)]
     with pytest.raises(ValueError):
         N.describe_variant(N.SP_F64, 9)
+
+
+def test_cuda_engine_default_depth():
+    """SlabRunner(depth=None) asks the engine (the method sat on PeerBuffer)."""
+    from paper_0912_4506_b200.dist import CudaEngine
+    from paper_0912_4506_b200.pipeline import DEFAULT_DEPTH
+    from paper_0912_4506_b200 import _native as N
+
+    class G:
+        sp_dtype = N.SP_F64
+    assert CudaEngine().default_depth(G()) == DEFAULT_DEPTH[N.SP_F64]
+    G.sp_dtype = N.SP_F32
+    assert CudaEngine().default_depth(G()) == DEFAULT_DEPTH[N.SP_F32]
