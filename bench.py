@@ -167,7 +167,85 @@ def cpu_sample(shape_full, kind, faces, dtype, budget_s=10.0, planes=64, sweeps_
     return lups / dt / 1e9, O.num_threads(), sample
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def reference_variants(shape_full, dt, T, budget_s=10.0):
+    """The reference package's OWN CPU code (stencilpipe, installed unmodified
+    into baseline/_ref by `pip install --target baseline/_ref`), timed like
+    its bench (R/bench.py:125-156: allocate + one untimed warm-up sweep, then
+    repeat until ``budget_s`` has elapsed) on a z-slab of the workload.  The
+    four variants SURVEY 8(d) names: sweep_naive and sweep_spatial_blocked
+    (numpy ufuncs: one core), run_node_sweeps with PipelineConfig(1, C, 1)
+    (the paper's pipelined scheme at full width, C = host cores) and with
+    PipelineConfig(1, 1, T) (the GPU's depth)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "stencilpipe")):
+        return {"unavailable": "baseline/_ref not installed (pip install --target baseline/_ref)"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    import numpy as np
+    from stencilpipe.grid import FillPattern, GridDims, allocate
+    from stencilpipe.kernel import sweep_naive, sweep_spatial_blocked
+    from stencilpipe.pipeline import PipelineConfig, default_block_size, run_node_sweeps
+
+    cores = len(os.sched_getaffinity(0))
+    nz, ny, nx = shape_full
+    wide = max(2, min(cores, 64))
+    planes = min(nz, max(32, wide))
+    dims = GridDims(nx, ny, planes)
+    cells = nx * ny * planes
+
+    def grid():
+        g = allocate(dims, "twogrid", FillPattern.random(0))
+        if dt == "f32":                          # numpy keeps f32 arithmetic in f32 (NEP 50)
+            g.a = g.a.astype(np.float32)
+            g.b = g.a.copy()
+        return g
+
+    def timed(name, one, levels_per_call, detail):
+        g = grid()
+        one(g)                                   # warm-up, untimed
+        t0 = time.monotonic()
+        calls = 0
+        while True:
+            one(g)
+            calls += 1
+            if time.monotonic() - t0 >= budget_s:
+                break
+        el = time.monotonic() - t0
+        return {"variant": name, "glups": round(cells * levels_per_call * calls / el / 1e9, 5),
+                "seconds": round(el, 2), "levels": levels_per_call * calls, "detail": detail}
+
+    rows = []
+    bs = (nx, ny, 16)
+    rows.append(timed("naive", sweep_naive, 1, "sweep_naive (R/kernel.py:43-47), 1 core"))
+    rows.append(timed("blocked", lambda g: sweep_spatial_blocked(g, bs), 1,
+                      f"sweep_spatial_blocked bs={bs} (R/kernel.py:59-80), 1 core"))
+    for label, cfg in ((f"pipeline(1,{wide},1)", PipelineConfig(teams=1, team_size=wide, updates_per_thread=1)),
+                       (f"pipeline(1,1,{T})", PipelineConfig(teams=1, team_size=1, updates_per_thread=T))):
+        cfg = PipelineConfig(teams=cfg.teams, team_size=cfg.team_size, updates_per_thread=cfg.updates_per_thread,
+                             block=default_block_size(dims, cfg))
+        rows.append(timed(label, lambda g, c=cfg: run_node_sweeps(g, c, 1), cfg.levels_per_sweep,
+                          f"run_node_sweeps {label} block={cfg.block} (R/pipeline.py:459-462), "
+                          f"{cfg.n_threads} threads"))
+    return {"sample": f"{nx}x{ny}x{planes} z-slab (random(0) fill), {budget_s:.0f} s per variant",
+            "cores": cores, "cpu_model": cpu_model(), "variants": rows}
+
+
 def run_reference_arm(args, rank):
+    """The reference arm: the reference algorithm's CPU implementation on this
+    host.  Reported value: the C port of sweep_naive (oracle/, all host
+    threads; faster than the reference's numpy code), timed >= 5 s per run;
+    beside it the reference package's own code (reference_variants)."""
     if rank != 0:
         return 0
     shape, kind, faces, dt, sweeps, desc, strong = WORKLOADS[args.workload]
@@ -180,7 +258,12 @@ def run_reference_arm(args, rank):
     planes = 32
     g = O.CGrid((planes, ny, nx), O.BoxPattern(kind, seed=0, faces=faces, global_shape=shape),
                 dtype=np.float64 if dt == "f64" else np.float32)
-    per_step = 2   # sweeps of the slab per step (bounded sample)
+    # sweeps of the slab per step: enough that the K timed steps take >= 5 s
+    g.sweeps(1)                                   # first touch, thread start-up
+    t0 = time.monotonic()
+    g.sweeps(2)
+    one = max((time.monotonic() - t0) / 2, 1e-3)
+    per_step = max(2, int(np.ceil(6.0 / (one * max(args.steps, 1)))))
     for _ in range(args.warmup):
         g.sweeps(per_step)
     t0 = time.monotonic()
@@ -190,16 +273,19 @@ def run_reference_arm(args, rank):
     lups = nx * ny * planes * per_step * args.steps
     v = lups / el / 1e9
     cores = O.num_threads()
-    sample = (f"{nx}x{ny}x{planes} z-slab of {args.workload} ({per_step} sweeps per step), "
+    sample = (f"{nx}x{ny}x{planes} z-slab of {args.workload} ({per_step} sweeps per step, {el:.1f} s timed), "
               f"oracle C port of sweep_naive (R/kernel.py:43-47) on {cores} threads")
+    T = args.depth or (C5_DEPTH if args.workload.startswith("c5") else 2)
+    variants = reference_variants(shape, dt, T, budget_s=args.cpu_seconds) if not args.no_cpu else None
     line = {
         "metric": "GLUP/s", "value": round(v, 3), "unit": "GLUP/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(el / args.steps * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+        "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
         "config": {"workload": desc, "sample": sample},
         "cpu_baseline": {"value": round(v, 3), "unit": "GLUP/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
+        "reference_package": variants,
         "e2e": {"value": round(v, 3), "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -55,17 +55,25 @@ def block_edges(extent: int, block: int) -> list[int]:
 def sweep_spatial_blocked(grid: TwoGrid, bs: tuple[int, int, int]) -> None:
     """Spatially blocked sweep (R/kernel.py:59-80).
 
-    The block size is validated exactly as the reference does; the device
-    kernel's own x-y tiles with z-marching are the spatial blocking, so the
-    sweep is one K1 launch -- bitwise equal to ``sweep_naive`` because the
-    per-cell arithmetic is unchanged (reference test_kernel.py:63-92).
+    The block size is validated exactly as the reference does.  The
+    reference's outer z loop over blocks becomes one single-level launch per
+    z-block (blocks in z order, like the reference's traversal); its inner
+    y/x blocks are the device kernel's own x-y tiles, which every launch
+    marches through z.  Every launch reads ``current`` and writes ``other``,
+    so the result is bitwise equal to ``sweep_naive`` (the per-cell
+    arithmetic is unchanged; reference test_kernel.py:63-92).
     """
     _require_device_grid(grid)
     d = grid.dims
-    for b, n in zip(bs, (d.nx, d.ny, d.nz)):
+    bx, by, bz = bs
+    for b, n in zip((bx, by, bz), (d.nx, d.ny, d.nz)):
         if not 1 <= b <= n:
             raise GridError(f"block size {bs} outside interior extents")
-    sweep_naive(grid)
+    ez = block_edges(d.nz, bz)
+    src, dst = grid.current_buffer(), grid.other_buffer()
+    for z0, z1 in zip(ez[:-1], ez[1:]):
+        _update(grid, src, dst, (z0, 0, 0), (z1, d.ny, d.nx))
+    grid.swap()
 
 
 def update_block(grid: TwoGrid, lo, hi, level: int = 1, direction: int = -1) -> None:

@@ -32,7 +32,7 @@ def _free():
 
 
 @pytest.mark.parametrize("name,depths", [("c1", [4]), ("c2", [1, 2, 4, 8]),
-                                         ("c3", [1, 2, 3, 4]), ("c5w", [4]),
+                                         ("c3", [1, 2, 3, 4]), ("c3", [5, 6, 8]), ("c5w", [1, 4, 8]),
                                          ("c4", [4, 8]), ("c5s", [2])])
 def test_baseline_config_digest(sp, big_digests, name, depths):
     for depth in depths:
@@ -45,7 +45,7 @@ def test_baseline_config_digest(sp, big_digests, name, depths):
         _free()
 
 
-@pytest.mark.parametrize("P,h", [(2, 4), (4, 2)])
+@pytest.mark.parametrize("P,h", [(2, 4), (4, 2), (2, 8), (8, 1)])
 def test_c5_strong_zslabs_match_single_grid(sp, big_digests, P, h):
     """C5 strong scaling: the 1024x1024x2048 global grid as P z-slabs with
     depth-h halos (ranks share the GPU, exchange by device copies); the slab
@@ -68,4 +68,20 @@ def test_c5_strong_zslabs_match_single_grid(sp, big_digests, P, h):
         total = (total + g.digest(index_base=z0 * ny * nx)) % (1 << 64)
     assert total == int(c["digests"]["100"])
     del grids
+    _free()
+
+
+@pytest.mark.parametrize("depth", [2, 3])
+def test_c3_compressed_storage_digest(sp, big_digests, depth):
+    """C3 (1024^3 fp64, 100 sweeps) in compressed single-array storage: the
+    in-place passes (K2-IP) reproduce the two-grid golden bit for bit."""
+    c = big_digests["c3"]
+    nz, ny, nx = c["shape"]
+    pat = sp.FillPattern.dirichlet_box(c["kind"], (nz, ny, nx), tuple(c["faces"]), seed=0)
+    g = sp.CompressedGrid(sp.GridDims(nx, ny, nz), pat)
+    assert g.digest() == int(c["digests"]["0"])
+    assert g.hbm_bytes < 0.7 * 2 * 8 * (nz + 2) * (ny + 2) * (nx + 2)
+    sp.sweeps(g, 100, depth=depth)
+    assert g.digest() == int(c["digests"]["100"]), depth
+    del g
     _free()
