@@ -203,6 +203,14 @@ int sp_sweep_tb_inplace(void* buf, int dtype, const sp_layout* L, int T, const i
 int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, void* stream);
 int64_t sp_ghost_shell_elems(int64_t nx, int64_t ny, int64_t nz);
 
+/* Scatter only the ghost face cells adjacent to the interior box [lo, hi)
+ * (z, y, x): a face only where the box touches it (lo == 0 / hi == n on that
+ * axis), within the box's extent on the other axes, edges and corners never.
+ * Replaces _refresh_compressed_ghosts (R/kernel.py:83-102) before a
+ * compressed update_block (R/kernel.py:124-147). */
+int sp_ghost_shell_region(void* base, int dtype, const sp_layout* L, const void* shell, const int64_t lo[3],
+                          const int64_t hi[3], void* stream);
+
 /* Introspection (benchmarks, reports): the kernel variant a temporally blocked
  * pass of depth T in dtype runs (after any sp_set_tuning override and the
  * fallback for variants not built for T), and a one-line description of it

@@ -586,12 +586,25 @@ int sp_sweep_tb_inplace(void* buf, int dtype, const sp_layout* L, int T, const i
 
 int64_t sp_ghost_shell_elems(int64_t nx, int64_t ny, int64_t nz);
 
-int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, void* stream) {
+namespace {
+int ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, const int64_t* rlo,
+                const int64_t* rhi, void* stream) {
     int rc = check_layout(L, dtype);
     if (rc) return rc;
     if (!base || !shell) return fail(SP_ERR_ARG, "null argument");
     if (L->gx != 1 || L->gy != 1 || L->gz != 1) return fail(SP_ERR_GRID, "ghost shell needs ghost depth 1");
-    sp::Shell g{L->nx, L->ny, L->nz, L->py, L->pz, L->origin, to_grid ? 1 : 0};
+    sp::Shell g{L->nx, L->ny, L->nz, L->py, L->pz, L->origin, to_grid ? 1 : 0, rlo ? 1 : 0, {0, 0, 0},
+                {L->nz, L->ny, L->nx}};
+    if (rlo) {
+        const int64_t n[3] = {L->nz, L->ny, L->nx};
+        for (int d = 0; d < 3; ++d) {
+            if (rlo[d] < 0 || rlo[d] > rhi[d] || rhi[d] > n[d])
+                return fail(SP_ERR_GRID, "refresh region outside the interior (axis %d: [%lld, %lld) of %lld)", d,
+                            (long long)rlo[d], (long long)rhi[d], (long long)n[d]);
+            g.rlo[d] = rlo[d];
+            g.rhi[d] = rhi[d];
+        }
+    }
     const int64_t total = sp_ghost_shell_elems(L->nx, L->ny, L->nz);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, 148 * 8));
     cudaStream_t s = (cudaStream_t)stream;
@@ -601,6 +614,17 @@ int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int t
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "ghost_shell_kernel launch");
     return SP_OK;
+}
+}  // namespace
+
+int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, void* stream) {
+    return ghost_shell(base, dtype, L, shell, to_grid, nullptr, nullptr, stream);
+}
+
+int sp_ghost_shell_region(void* base, int dtype, const sp_layout* L, const void* shell, const int64_t lo[3],
+                          const int64_t hi[3], void* stream) {
+    if (!lo || !hi) return fail(SP_ERR_ARG, "null region");
+    return ghost_shell(base, dtype, L, const_cast<void*>(shell), 1, lo, hi, stream);
 }
 
 int64_t sp_ghost_shell_elems(int64_t nx, int64_t ny, int64_t nz) {

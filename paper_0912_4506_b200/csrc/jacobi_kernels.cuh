@@ -1081,7 +1081,33 @@ __global__ void __launch_bounds__(256) row_copy_kernel(const R* __restrict__ src
 struct Shell {
     int64_t nx, ny, nz, py, pz, origin;
     int to_grid;   // 1: shell -> grid, 0: grid -> shell
+    // region scatter (to_grid only): just the face cells adjacent to the box
+    // [rlo, rhi) -- a face only if the region touches it, within the region's
+    // extent on the other two axes (R/kernel.py:83-102's refresh)
+    int region;
+    int64_t rlo[3], rhi[3];   // (z, y, x)
 };
+
+// face cell (exactly one coordinate outside [0, n)) adjacent to the region?
+__device__ __forceinline__ bool shell_in_region(const Shell& g, int64_t z, int64_t y, int64_t x) {
+    const int64_t c[3] = {z, y, x}, n[3] = {g.nz, g.ny, g.nx};
+    int out = -1;
+    for (int d = 0; d < 3; ++d) {
+        if (c[d] < 0 || c[d] >= n[d]) {
+            if (out >= 0) return false;   // edge / corner: never part of a face refresh
+            out = d;
+        }
+    }
+    if (out < 0) return false;
+    for (int d = 0; d < 3; ++d) {
+        if (d == out) {
+            if (c[d] < 0 ? g.rlo[d] != 0 : g.rhi[d] != n[d]) return false;
+        } else if (c[d] < g.rlo[d] || c[d] >= g.rhi[d]) {
+            return false;
+        }
+    }
+    return true;
+}
 
 template <typename R>
 __global__ void __launch_bounds__(256) ghost_shell_kernel(R* base, R* shell, const Shell g) {
@@ -1105,6 +1131,7 @@ __global__ void __launch_bounds__(256) ghost_shell_kernel(R* base, R* shell, con
             else { y = (f - 2 * W) >> 1; x = ((f - 2 * W) & 1) ? g.nx : -1; }
         }
         R* cell = base + g.origin + z * g.pz + y * g.py + x;
+        if (g.region && !shell_in_region(g, z, y, x)) continue;
         if (g.to_grid) *cell = shell[i];
         else shell[i] = *cell;
     }

@@ -335,15 +335,30 @@ class CompressedGrid:
 
     The reference shifts its box one cell diagonally per level and refreshes
     the ghost faces before each block update (R/kernel.py:83-121).  On the
-    device every pass of depth T runs in place (``sp_sweep_tb_inplace``):
-    z-chunks of ``chunk`` planes go in order and store their level-T planes
-    2*chunk+T planes away from where they read them -- down when ascending,
-    up when descending -- so a chunk only overwrites planes that chunks two
-    and three back have finished reading (device counters enforce it).  The
-    box therefore moves by whole planes in z (``offset``); x/y stay put.  The
-    ghost shell is packed once (``sp_ghost_shell``) and re-scattered after
-    every pass.  HBM: (nz + 2 + slack) planes instead of 2 (nz + 2), with
-    slack = 4*chunk + 16 (any T <= 8, either direction from any offset).
+    device the box moves by whole planes in z (``offset``, in planes); x/y
+    stay put, so the logical content -- ``interior()``, ``value_at``,
+    ``full_view`` at any offset -- is what the reference's diagonal shift
+    gives.  Two ways to size the slack:
+
+    * ``slack=None`` (device-native, the memory-saving form): every pass of
+      depth T runs IN PLACE (``sp_sweep_tb_inplace``): z-chunks of ``chunk``
+      planes go in order and store their level-T planes 2*chunk+T planes away
+      from where they read them -- down when ascending, up when descending --
+      so a chunk only overwrites planes that chunks two and three back have
+      finished reading (device counters enforce it).  The ghost shell is
+      packed once (``sp_ghost_shell``) and re-scattered after every pass.
+      HBM: (nz + 2 + slack) planes instead of 2 (nz + 2), slack = 4*chunk + 16.
+    * ``slack=S`` (the reference's contract, honoured as given): the box
+      starts at offset S and moves like the reference's -- ``shift_origin``
+      within [0, S], ``update_block(level, direction)`` reads at
+      offset + direction*(level-1) and writes one cell off, node sweeps of U
+      levels move it by -U / +U (R/pipeline.py:349-387), needing S >= U.  The
+      layout is the reference's too: S extra cells on every axis and the box
+      shifted DIAGONALLY, which is what keeps a forward blocked traversal from
+      overwriting cells later blocks still read.  Those moves are smaller
+      than an in-place pass needs, so each level (or pass) is computed into a
+      scratch box and copied to the shifted position, as the reference
+      materialises each right-hand side.
     """
 
     storage = "compressed"
@@ -364,19 +379,29 @@ class CompressedGrid:
         self.device = dev
         self.chunk = max(16, min(int(chunk), dims.nz))     # >= 2T for every T <= 8
         smax = 2 * self.chunk + 8
-        need = 2 * smax
-        if slack is not None and slack < 0:
-            raise GridError(f"slack must be >= 0, got {slack}")
-        self.slack = max(need, int(slack or 0))
+        if slack is None:
+            self.reference_slack = False
+            self.slack = 2 * smax
+            offset0 = smax
+        else:
+            if slack < 0:
+                raise GridError(f"slack must be >= 0, got {slack}")
+            if max(n + 2 + int(slack) for n in dims.shape) ** 3 > np.iinfo(np.int64).max // 8:
+                raise GridError("compressed allocation overflows address arithmetic")   # R/grid.py:180-181
+            self.reference_slack = True
+            self.slack = int(slack)
+            offset0 = self.slack                        # R/grid.py:185
         lay = N.Layout()
         n_alloc = ctypes.c_int64()
-        N.check(L.sp_layout_make(dims.nx, dims.ny, dims.nz + self.slack, 1, 1, 1, self.sp_dtype,
+        sxy = self.slack if self.reference_slack else 0  # reference: slack on every axis
+        N.check(L.sp_layout_make(dims.nx + sxy, dims.ny + sxy, dims.nz + self.slack, 1, 1, 1, self.sp_dtype,
                                  ctypes.byref(lay), ctypes.byref(n_alloc)))
         self.blayout = lay                               # the whole allocation
-        self.layout = N.Layout(*lay.as_tuple())          # the box, relative to box_base()
-        self.layout.nz = dims.nz
-        self.offset = smax                               # box plane z sits at allocation plane z + offset
+        self.layout = N.Layout(*lay.as_tuple())          # the box at offset 0 (native: relative to _box_ptr)
+        self.layout.nx, self.layout.ny, self.layout.nz = dims.nx, dims.ny, dims.nz
+        self.offset = offset0                            # box plane z sits at allocation plane z + offset
         self._ascend_next = True
+        self._scratch_buf = None
         with torch.cuda.device(self.device):
             self._buf = torch.zeros(n_alloc.value, dtype=self.torch_dtype, device=self.device)
             nshell = L.sp_ghost_shell_elems(dims.nx, dims.ny, dims.nz)
@@ -384,9 +409,7 @@ class CompressedGrid:
             nch = -(-dims.nz // self.chunk)
             self._counters = torch.zeros(nch, dtype=torch.int32, device=self.device)
         self._fill(pattern)
-        with _on(self.device):
-            N.check(L.sp_ghost_shell(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
-                                     ctypes.c_void_p(self._shell.data_ptr()), 0, self.stream()))
+        self._gather_shell()
 
     # -- storage -------------------------------------------------------------
 
@@ -394,20 +417,38 @@ class CompressedGrid:
         import torch
         return ctypes.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
 
-    def _box_ptr(self):
-        """Base pointer under which ``layout`` describes the box at the current offset."""
+    def _at(self, offset: int | None = None):
+        """(base pointer, layout) of the box at ``offset`` (default: current).
+        Native: the box slides in z (pointer moves, layout fixed); reference
+        slack: it slides diagonally (layout origin moves by o*(pz + py + 1))."""
+        o = self.offset if offset is None else offset
         es = self._buf.element_size()
-        return ctypes.c_void_p(self._buf.data_ptr() + self.offset * self.blayout.pz * es)
+        if self.reference_slack:
+            # z and y by the pointer (whole rows keep it 16-byte aligned for TMA), x by the origin
+            lay = N.Layout(*self.layout.as_tuple())
+            lay.origin += o
+            return ctypes.c_void_p(self._buf.data_ptr() + o * (lay.pz + lay.py) * es), lay
+        return ctypes.c_void_p(self._buf.data_ptr() + o * self.blayout.pz * es), self.layout
+
+    def _box_ptr(self, offset: int | None = None):
+        return self._at(offset)[0]
+
+    def _box_start(self, offset: int | None = None) -> int:
+        """Element index of the box's ghost corner (z=-1, y=-1, x=-1) in the allocation."""
+        o = self.offset if offset is None else offset
+        lay = self.layout
+        diag = o * (lay.pz + lay.py + 1) if self.reference_slack else o * lay.pz   # as _at() places it
+        return lay.origin + diag - lay.pz - lay.py - 1
 
     def _box_view(self):
-        lay, d = self.blayout, self.dims
-        off = lay.origin + (self.offset - 1) * lay.pz - lay.py - 1
-        return self._buf.as_strided((d.nz + 2, d.ny + 2, d.nx + 2), (lay.pz, lay.py, 1), off)
+        lay, d = self.layout, self.dims
+        return self._buf.as_strided((d.nz + 2, d.ny + 2, d.nx + 2), (lay.pz, lay.py, 1), self._box_start())
 
     def _fill(self, pattern):
         if isinstance(pattern, FillPattern):
+            ptr, lay = self._at()
             with _on(self.device):
-                N.check(N.lib().sp_fill(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
+                N.check(N.lib().sp_fill(ptr, self.sp_dtype, ctypes.byref(lay),
                                         ctypes.byref(pattern.to_c()), self.stream()))
             return
         if not hasattr(pattern, "evaluate"):
@@ -416,6 +457,22 @@ class CompressedGrid:
         d = self.dims
         vals = np.asarray(pattern.evaluate((-1, -1, -1), (d.nz + 1, d.ny + 1, d.nx + 1)), dtype=self.dtype)
         self._box_view().copy_(torch.from_numpy(np.ascontiguousarray(vals)))
+
+    def _gather_shell(self):
+        """Pack the box's ghost shell (the Dirichlet values, fixed for the run)."""
+        ptr, lay = self._at()
+        with _on(self.device):
+            N.check(N.lib().sp_ghost_shell(ptr, self.sp_dtype, ctypes.byref(lay),
+                                           ctypes.c_void_p(self._shell.data_ptr()), 0, self.stream()))
+        self._ghosts_at = self.offset
+
+    def _scatter_shell(self, offset: int | None = None):
+        o = self.offset if offset is None else offset
+        ptr, lay = self._at(o)
+        with _on(self.device):
+            N.check(N.lib().sp_ghost_shell(ptr, self.sp_dtype, ctypes.byref(lay),
+                                           ctypes.c_void_p(self._shell.data_ptr()), 1, self.stream()))
+        self._ghosts_at = o
 
     @property
     def buffers(self):
@@ -426,17 +483,115 @@ class CompressedGrid:
         """The ghosted box (device view) at the current offset."""
         return self._box_view()
 
+    def shift_origin(self, delta: int) -> None:
+        """Move the box origin by ``delta`` planes without moving data (R/grid.py:191-195)."""
+        new = self.offset + int(delta)
+        if not 0 <= new <= self.slack:
+            raise GridError(f"origin offset {new} escapes slack [0, {self.slack}]")
+        self.offset = new
+
     # -- passes --------------------------------------------------------------
 
-    def run_passes(self, levels: int, depth: int) -> None:
-        """``levels`` levels as in-place passes of ``depth`` (stream-ordered)."""
+    def _scratch(self):
+        """A box-sized buffer in the box layout (out-of-place levels; allocated on first use)."""
+        import torch
+        if self._scratch_buf is None:
+            n = (self.dims.nz + 2) * self.blayout.pz
+            with torch.cuda.device(self.device):
+                self._scratch_buf = torch.empty(n, dtype=self.torch_dtype, device=self.device)
+        return self._scratch_buf
+
+    def _pass_shifted(self, T: int, o_read: int, o_write: int, lo, hi) -> None:
+        """T levels over the interior box [lo, hi) read at ``o_read`` (walls on the
+        box faces: its ghost cells hold the level's boundary) into the scratch box,
+        then those cells into the box at ``o_write`` -- the reference's
+        materialised right-hand side (R/kernel.py:105-121)."""
+        if any(h <= l for l, h in zip(lo, hi)):
+            return
+        scr = self._scratch()
+        ptr, lay = self._at(o_read)
+        # the scratch holds the box with its ghost corner at element 0, same pitches
+        es = self._buf.element_size()
+        scr_base = ctypes.c_void_p(scr.data_ptr() - (lay.origin - lay.pz - lay.py - 1) * es)
+        with _on(self.device):
+            N.check(N.lib().sp_sweep_tb(ptr, scr_base, self.sp_dtype, ctypes.byref(lay), int(T),
+                                        N.i64x3(lo), N.i64x3(hi), None, None, self.stream()))
+        shape = tuple(h - l for l, h in zip(lo, hi))
+        strides = (lay.pz, lay.py, 1)
+        rel = (lo[0] + 1) * lay.pz + (lo[1] + 1) * lay.py + (lo[2] + 1)   # from the ghost corner
+        src = scr.as_strided(shape, strides, rel)
+        dst = self._buf.as_strided(shape, strides, self._box_start(o_write) + rel)
+        dst.copy_(src)
+
+    def update_block(self, lo, hi, level: int = 1, direction: int = -1) -> None:
+        """One level over the interior box [lo, hi) (R/kernel.py:141-147): read at
+        offset + direction*(level-1), refresh the ghost faces the box touches
+        there (R/kernel.py:83-102), write one plane off in ``direction``.
+        Origin bookkeeping is the caller's (``shift_origin``), as in the reference."""
+        if direction not in (-1, 1):
+            raise GridError(f"direction must be -1 or +1, got {direction}")
+        lo, hi = tuple(int(v) for v in lo), tuple(int(v) for v in hi)
+        for l, h, n in zip(lo, hi, self.dims.shape):
+            if l > h:
+                raise GridError(f"malformed region {lo}..{hi}")
+            if l < 0 or h > n:
+                raise GridError(f"compressed update region {lo}..{hi} must lie inside the interior")
+        o_read = self.offset + direction * (level - 1)
+        o_write = o_read + direction
+        if not (0 <= o_read <= self.slack and 0 <= o_write <= self.slack):
+            raise GridError(f"level {level} in direction {direction} escapes slack [0, {self.slack}] "
+                            f"(read at {o_read}, write at {o_write})")
+        ptr, lay = self._at(o_read)
+        with _on(self.device):
+            N.check(N.lib().sp_ghost_shell_region(ptr, self.sp_dtype, ctypes.byref(lay),
+                                                  ctypes.c_void_p(self._shell.data_ptr()), N.i64x3(lo),
+                                                  N.i64x3(hi), self.stream()))
+        self._pass_shifted(1, o_read, o_write, lo, hi)
+
+    def node_sweep(self, U: int, depth: int, direction: int) -> None:
+        """U levels moving the origin by direction*U (R/pipeline.py:381-387), as
+        passes of ``depth`` through the scratch box (slack given as in the reference)."""
+        from .pipeline import ScheduleError
+        end = self.offset + direction * U
+        if not 0 <= end <= self.slack:
+            raise ScheduleError(f"node sweep of U={U} in direction {direction} from offset {self.offset} "
+                                f"escapes slack [0, {self.slack}]")
         d = self.dims
+        done = 0
+        while done < U:
+            T = min(depth, U - done)
+            self._scatter_shell()                          # the boundary at the read position
+            o_write = self.offset + direction * T
+            self._pass_shifted(T, self.offset, o_write, (0, 0, 0), d.shape)
+            self.offset = o_write
+            done += T
+
+    def run_passes(self, levels: int, depth: int) -> None:
+        """``levels`` levels as passes of ``depth`` (stream-ordered)."""
+        if self.reference_slack:
+            from .pipeline import ScheduleError
+            if self.offset - levels >= 0:
+                self.node_sweep(levels, depth, -1)
+            elif self.offset + levels <= self.slack:
+                self.node_sweep(levels, depth, 1)
+            else:
+                raise ScheduleError(f"{levels} levels do not fit the slack {self.slack} from offset "
+                                    f"{self.offset}")
+            self._scatter_shell()
+            return
+        d = self.dims
+        if self._ghosts_at != self.offset:
+            self._scatter_shell()
         done = 0
         while done < levels:
             T = min(depth, levels - done)
             s = 2 * min(self.chunk, d.nz) + T
             up_ok = self.offset - s >= 0
             down_ok = self.offset + s <= self.slack
+            if not (up_ok or down_ok):
+                from .pipeline import ScheduleError
+                raise ScheduleError(f"in-place pass needs {s} planes of slack on one side of offset "
+                                    f"{self.offset} (slack {self.slack})")
             ascend = up_ok if (self._ascend_next or not down_ok) else not down_ok
             lo = (self.offset, 0, 0)
             hi = (self.offset + d.nz, d.ny, d.nx)
@@ -445,9 +600,8 @@ class CompressedGrid:
                     ctypes.c_void_p(self._buf.data_ptr()), self.sp_dtype, ctypes.byref(self.blayout), int(T),
                     N.i64x3(lo), N.i64x3(hi), int(self.chunk), 1 if ascend else -1,
                     ctypes.c_void_p(self._counters.data_ptr()), self._counters.numel(), self.stream()))
-                self.offset += -s if ascend else s
-                N.check(N.lib().sp_ghost_shell(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
-                                               ctypes.c_void_p(self._shell.data_ptr()), 1, self.stream()))
+            self.offset += -s if ascend else s
+            self._scatter_shell()
             self._ascend_next = not ascend
             done += T
 
@@ -471,8 +625,9 @@ class CompressedGrid:
 
     def digest(self, index_base: int = 0) -> int:
         out = ctypes.c_uint64()
+        ptr, lay = self._at()
         with _on(self.device):
-            N.check(N.lib().sp_digest(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
+            N.check(N.lib().sp_digest(ptr, self.sp_dtype, ctypes.byref(lay),
                                       int(index_base), ctypes.byref(out), self.stream()))
         return int(out.value)
 
@@ -486,29 +641,52 @@ class CompressedGrid:
         d = self.dims
         return (d.nz + 2, d.ny + 2, d.nx + 2)
 
+    STAGING_PLANES = 64
+
+    def _staging(self):
+        """Bounded device staging buffer (STAGING_PLANES dense ghosted planes) for
+        host transfers: linear PCIe copies repacked on the device by K6, so no
+        box-sized temporary is ever made (the box view is strided)."""
+        import torch
+        if getattr(self, "_stg", None) is None:
+            hz, hy, hx = self.host_shape()
+            n = min(hz, self.STAGING_PLANES) * hy * hx
+            with torch.cuda.device(self.device):
+                self._stg = torch.empty(n, dtype=self.torch_dtype, device=self.device)
+        return ctypes.c_void_p(self._stg.data_ptr()), self._stg.numel()
+
     def upload(self, field, stream=None) -> None:
-        """Replace the box (ghosts included) with a host field of shape host_shape()."""
+        """Replace the box (ghosts included) with a host field of shape host_shape();
+        the packed ghost shell is re-gathered from it."""
         import torch
         t = field if isinstance(field, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(field))
-        if tuple(t.shape) != self.host_shape() or t.dtype != self.torch_dtype:
-            raise GridError(f"upload needs a {self.torch_dtype} field of shape {self.host_shape()}")
-        st = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
-        with torch.cuda.stream(st):
-            self._box_view().copy_(t, non_blocking=True)
-            with _on(self.device):
-                N.check(N.lib().sp_ghost_shell(self._box_ptr(), self.sp_dtype, ctypes.byref(self.layout),
-                                               ctypes.c_void_p(self._shell.data_ptr()), 0,
-                                               ctypes.c_void_p(st.cuda_stream)))
+        if tuple(t.shape) != self.host_shape() or t.dtype != self.torch_dtype or not t.is_contiguous():
+            raise GridError(f"upload needs a contiguous {self.torch_dtype} field of shape {self.host_shape()}")
+        s = self.stream() if stream is None else ctypes.c_void_p(stream)
+        stg, n_stg = self._staging()
+        ptr, lay = self._at()
+        with _on(self.device):
+            N.check(N.lib().sp_copy_in(ctypes.c_void_p(t.data_ptr()), self.sp_dtype, ctypes.byref(lay),
+                                       ptr, None, stg, n_stg, s))
+            N.check(N.lib().sp_ghost_shell(ptr, self.sp_dtype, ctypes.byref(lay),
+                                           ctypes.c_void_p(self._shell.data_ptr()), 0, s))
+        self._ghosts_at = self.offset
 
     def download(self, out=None, stream=None):
         """The interior into host memory (pass a pinned ``out`` for an asynchronous copy)."""
         import torch
+        d = self.dims
         fresh = out is None
         if fresh:
-            out = torch.empty(self.dims.shape, dtype=self.torch_dtype, pin_memory=True)
-        st = torch.cuda.current_stream(self.device) if stream is None else torch.cuda.ExternalStream(stream)
-        with torch.cuda.stream(st):
-            out.copy_(self.interior_device(), non_blocking=True)
+            out = torch.empty(d.shape, dtype=self.torch_dtype, pin_memory=True)
+        if tuple(out.shape) != tuple(d.shape) or out.dtype != self.torch_dtype or not out.is_contiguous():
+            raise GridError(f"download needs a contiguous {self.torch_dtype} tensor of shape {d.shape}")
+        s = self.stream() if stream is None else ctypes.c_void_p(stream)
+        stg, n_stg = self._staging()
+        ptr, lay = self._at()
+        with _on(self.device):
+            N.check(N.lib().sp_copy_out(ptr, self.sp_dtype, ctypes.byref(lay),
+                                        ctypes.c_void_p(out.data_ptr()), stg, n_stg, s))
         if fresh:
             torch.cuda.synchronize(self.device)
         return out
@@ -566,12 +744,13 @@ def load_field(fh) -> tuple[GridDims, np.ndarray]:
     return dims, flat.reshape(dims.alloc_shape)
 
 
-def allocate(dims: GridDims, mode: str, pattern, slack: int = 0, **kw):
-    """Allocate and initialise a device grid (R/grid.py:217-223)."""
+def allocate(dims: GridDims, mode: str, pattern, slack: int | None = None, **kw):
+    """Allocate and initialise a device grid (R/grid.py:217-223).
+
+    ``slack`` (compressed only) is honoured as given, as in the reference;
+    omitted, the device picks the slack its in-place passes need."""
     if mode == "twogrid":
         return TwoGrid(dims, pattern, **kw)
     if mode == "compressed":
-        if slack < 0:
-            raise GridError(f"slack must be >= 0, got {slack}")
-        return CompressedGrid(dims, pattern, slack=slack or None, **kw)
+        return CompressedGrid(dims, pattern, slack=slack, **kw)
     raise GridError(f"unknown storage mode {mode!r}")

@@ -13,7 +13,7 @@ from __future__ import annotations
 import ctypes
 
 from . import _native as N
-from .grid import GridError, TwoGrid, _on
+from .grid import CompressedGrid, GridError, TwoGrid, _on
 
 ONE_SIXTH = 1.0 / 6.0
 
@@ -77,12 +77,20 @@ def sweep_spatial_blocked(grid: TwoGrid, bs: tuple[int, int, int]) -> None:
 
 
 def update_block(grid: TwoGrid, lo, hi, level: int = 1, direction: int = -1) -> None:
-    """One region at one level; level parity picks src/dst, no swap (R/kernel.py:124-147)."""
-    _require_device_grid(grid)
-    d = grid.dims
+    """One region at one level (R/kernel.py:124-147).
+
+    Two-grid: level parity picks src/dst, no swap.  Compressed: reads at the
+    offset ``level`` implies relative to the current origin, refreshes the
+    ghost faces the region touches and writes one plane off in ``direction``
+    (CompressedGrid.update_block); origin bookkeeping is the caller's."""
     for l, h in zip(lo, hi):
         if l > h:
             raise GridError(f"malformed region {lo}..{hi}")
+    if isinstance(grid, CompressedGrid):
+        grid.update_block(lo, hi, level=level, direction=direction)
+        return
+    _require_device_grid(grid)
+    d = grid.dims
     for l, h, n in zip(lo, hi, d.shape):
         if l < -d.ghost + 1 or h > n + d.ghost - 1:
             raise GridError("region escapes allocation")

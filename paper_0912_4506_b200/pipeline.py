@@ -224,7 +224,15 @@ def run_node_sweeps(grid: TwoGrid, cfg: PipelineConfig, sweeps_: int,
     check_schedule(grid.dims, cfg, level_domains)
     depth = cfg.depth or DEFAULT_DEPTH[grid.sp_dtype]
     if compressed and level_domains is not None:
-        raise ScheduleError("compressed storage runs full-box node sweeps only (no level domains)")
+        raise ScheduleError("compressed storage supports interior domains only")   # R/pipeline.py:312-313
+    if compressed and grid.reference_slack:
+        # the reference's contract: slack >= U, origin -U / +U per node sweep (R/pipeline.py:308-311,349-387)
+        if grid.slack < U:
+            raise ScheduleError(f"compressed slack {grid.slack} < U={U}")
+        for k in range(sweeps_):
+            grid.node_sweep(U, depth, -1 if k % 2 == 0 else 1)
+        grid._scatter_shell()
+        return
     if level_domains is None:
         for _ in range(sweeps_):
             sweeps(grid, U, depth)
