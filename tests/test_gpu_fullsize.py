@@ -62,6 +62,15 @@ def test_c5_strong_zslabs_match_single_grid(sp, big_digests, P, h):
         exchange_halos_local(grids, d, h)
         for r, g in enumerate(grids):
             outer_step(g, d, r, cfg, h=h)
+    rem = levels % h          # h = 8: 12 steps of 8 levels, then a 4-level step on the same halo
+    if rem:
+        from paper_0912_4506_b200.decomp import face_flags
+        from paper_0912_4506_b200.pipeline import run_pass
+        exchange_halos_local(grids, d, h)
+        for r, g in enumerate(grids):
+            e_lo, e_hi = face_flags(d, r)
+            run_pass(g, rem, (0, 0, 0), g.dims.shape, e_lo, e_hi)
+            g.swap()
     total = 0
     for r, g in enumerate(grids):
         z0 = d.ranges(r)[0][0]
