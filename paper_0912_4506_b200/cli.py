@@ -12,10 +12,13 @@ and the device pass depth is ``--depth``.  Timing follows R/bench.py:125-156
 (allocation/init untimed, one warm-up sweep, median of ``--reps``) with CUDA
 events instead of ``time.monotonic``.
 
-Verification: against the reference package's own ``oracle`` when
-``stencilpipe`` is importable (``--reference-path``), otherwise against an
-independent device path (one-level K2 sweeps, the ``sweep_naive`` engine)
--- the latter checks temporal blocking, not the arithmetic itself.
+Verification: against the reference package's own code -- ``stencilpipe``
+from ``--reference-path``, from the unmodified install in ``baseline/_ref``,
+or from ``sys.path`` -- running ``sweep_naive`` on its own ``TwoGrid``
+(R/verify.py:16-21; arrays cast to float32 for ``--dtype float32``, which
+numpy keeps in float32, so both dtypes are checked bit for bit).  Without the
+reference package ``verify``/``dist`` exit with status 2 and ``bench``
+reports "skipped": the device is never compared with itself.
 """
 
 from __future__ import annotations
@@ -30,7 +33,7 @@ import numpy as np
 from .grid import FillPattern, GridDims, allocate
 from .kernel import sweep_naive, sweep_spatial_blocked
 from .pipeline import PipelineConfig, default_block_size, run_node_sweeps, sweeps
-from .verify import REL_TOL, compare
+from .verify import F32_REL_TOL, REL_TOL, compare
 
 COLUMNS = ("variant", "nx", "ny", "nz", "n", "t", "T", "dl", "du", "dt",
            "sync", "storage", "sweeps", "seconds", "mlups", "verified")
@@ -133,6 +136,9 @@ def _run_variant(variant, dims, pattern, cfg, n_sweeps, dtype):
     if variant == "pipeline":
         if cfg.block is None:
             cfg = replace(cfg, block=default_block_size(dims, cfg))
+        if cfg.storage == "compressed":
+            # warm-up plus timed run shift the origin by up to two node sweeps (R/bench.py:147-150)
+            grid = allocate(dims, "compressed", pattern, slack=2 * cfg.levels_per_sweep, dtype=dtype)
         run_node_sweeps(grid, cfg, 1)
         sec = _timed(lambda: run_node_sweeps(grid, cfg, n_sweeps))
         return grid, interior * n_sweeps * cfg.levels_per_sweep, sec
@@ -145,23 +151,44 @@ def _levels(variant, cfg, total_sweeps):
     return total_sweeps + 1
 
 
-def _reference_field(args, dims, pattern, levels, dtype):
-    """Interior after ``levels`` sweeps: the reference oracle if importable, else
-    the independent one-level device engine."""
-    if args.reference_path:
-        sys.path.insert(0, args.reference_path)
+class ReferenceUnavailable(RuntimeError):
+    """The reference package (stencilpipe) is not importable: nothing to verify against."""
+
+
+def _import_reference(args):
+    import os
+    roots = [args.reference_path] if getattr(args, "reference_path", None) else []
+    roots.append(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref"))
+    for r in roots:
+        if r and os.path.isdir(os.path.join(r, "stencilpipe")) and r not in sys.path:
+            sys.path.insert(0, r)
     try:
         import stencilpipe.grid as rg
-        from stencilpipe.verify import oracle
-        rp = {"constant": lambda: rg.FillPattern.constant(args.value),
-              "linear": rg.FillPattern.linear, "hotplate": rg.FillPattern.hotplate,
-              "random": lambda: rg.FillPattern.random(args.seed)}[args.pattern]()
-        g = oracle(rg.GridDims(dims.nx, dims.ny, dims.nz), rp, levels)
-        return g.interior().astype(dtype), "reference"
-    except ImportError:
-        g = allocate(dims, "twogrid", pattern, dtype=dtype)
-        sweeps(g, levels, depth=1)
-        return g.interior(), "device-naive"
+        import stencilpipe.kernel as rk
+    except ImportError as exc:
+        raise ReferenceUnavailable("verification needs the reference package stencilpipe "
+                                   "(--reference-path DIR, or install it into baseline/_ref)") from exc
+    return rg, rk
+
+
+def _reference_field(args, dims, pattern, levels, dtype):
+    """Interior after ``levels`` naive sweeps by the reference package's own code
+    (its TwoGrid + sweep_naive = R/verify.py:16-21's oracle), in ``dtype``."""
+    rg, rk = _import_reference(args)
+    rp = {"constant": lambda: rg.FillPattern.constant(args.value),
+          "linear": rg.FillPattern.linear, "hotplate": rg.FillPattern.hotplate,
+          "random": lambda: rg.FillPattern.random(args.seed)}[args.pattern]()
+    g = rg.allocate(rg.GridDims(dims.nx, dims.ny, dims.nz), "twogrid", rp)
+    if dtype == np.float32:
+        g.a = g.a.astype(np.float32)
+        g.b = g.a.copy()
+    for _ in range(levels):
+        rk.sweep_naive(g)
+    return np.ascontiguousarray(g.interior()), "reference"
+
+
+def _tol(dtype):
+    return REL_TOL if dtype == np.float64 else F32_REL_TOL
 
 
 def cmd_bench(args) -> int:
@@ -176,21 +203,32 @@ def cmd_bench(args) -> int:
         seconds, updates, grid = runs[len(runs) // 2]
         verified = "skipped"
         if not args.no_verify and max(dims.shape) <= 64:
-            ref, _ = _reference_field(args, dims, pattern, _levels(variant, cfg, args.sweeps), dtype)
-            verified = "yes" if compare(ref, grid, tol=REL_TOL if dtype == np.float64 else 1e-5).passed else "no"
+            try:
+                ref, _ = _reference_field(args, dims, pattern, _levels(variant, cfg, args.sweeps), dtype)
+                verified = "yes" if compare(ref, grid, tol=_tol(dtype)).passed else "no"
+            except ReferenceUnavailable:
+                verified = "skipped"
         results.append(BenchResult("gpu-" + variant, dims, cfg, args.sweeps, seconds, updates, verified))
     sys.stdout.write(report(results, args.format))
     return 1 if any(r.verified == "no" for r in results) else 0
 
 
 def cmd_verify(args) -> int:
+    """R/bench.py:194-207: node sweeps on the device against the reference's oracle."""
     dims, pattern, cfg, dtype = _dims(args), _pattern(args), _config(args), _dtype(args)
-    grid = allocate(dims, "twogrid", pattern, dtype=dtype)
+    if cfg.block is None:
+        cfg = replace(cfg, block=default_block_size(dims, cfg))
+    slack = cfg.levels_per_sweep if cfg.storage == "compressed" else None
+    grid = allocate(dims, cfg.storage, pattern, slack=slack, dtype=dtype)
     run_node_sweeps(grid, cfg, args.sweeps)
-    ref, source = _reference_field(args, dims, pattern, args.sweeps * cfg.levels_per_sweep, dtype)
-    cmp = compare(ref, grid)
-    print(f"verify gpu/{source} U={cfg.levels_per_sweep} depth={cfg.depth or 'auto'} "
-          f"sweeps={args.sweeps}: {cmp}")
+    try:
+        ref, source = _reference_field(args, dims, pattern, args.sweeps * cfg.levels_per_sweep, dtype)
+    except ReferenceUnavailable as exc:
+        print(f"verify: {exc}", file=sys.stderr)
+        return 2
+    cmp = compare(ref, grid, tol=_tol(dtype))
+    print(f"verify gpu-{cfg.storage}/{source} n={cfg.teams} t={cfg.team_size} T={cfg.updates_per_thread} "
+          f"depth={cfg.depth or 'auto'} sweeps={args.sweeps}: {cmp}")
     return 0 if cmp.passed else 1
 
 
@@ -199,8 +237,12 @@ def cmd_dist(args) -> int:
     dims, pattern, cfg, dtype = _dims(args), _pattern(args), _config(args), _dtype(args)
     gathered, _ = run_distributed(dims, pattern, args.layout, cfg, args.outer_steps, dtype=dtype)
     levels = args.outer_steps * cfg.levels_per_sweep
-    ref, source = _reference_field(args, dims, pattern, levels, dtype)
-    cmp = compare(ref, gathered)
+    try:
+        ref, source = _reference_field(args, dims, pattern, levels, dtype)
+    except ReferenceUnavailable as exc:
+        print(f"dist: {exc}", file=sys.stderr)
+        return 2
+    cmp = compare(ref, gathered, tol=_tol(dtype))
     print(f"dist layout={'x'.join(map(str, args.layout))} h={cfg.levels_per_sweep} "
           f"steps={args.outer_steps} ({source}): {cmp}")
     return 0 if cmp.passed else 1
@@ -217,7 +259,7 @@ def _add_config_flags(p):
     p.add_argument("--dt", type=int, default=0)
     p.add_argument("--block", type=_parse_triple, default=None)
     p.add_argument("--sync", choices=("barrier", "relaxed"), default="relaxed")
-    p.add_argument("--storage", choices=("twogrid",), default="twogrid")
+    p.add_argument("--storage", choices=("twogrid", "compressed"), default="twogrid")
     p.add_argument("--pattern", choices=("constant", "linear", "hotplate", "random"), default="random")
     p.add_argument("--value", type=float, default=0.0)
     p.add_argument("--seed", type=int, default=42)

@@ -39,8 +39,79 @@ def test_cli_bench_verify_dist_on_gpu():
     lines = out.getvalue().splitlines()
     assert lines[1].startswith("gpu-naive") and lines[1].endswith(",yes")
     assert lines[2].startswith("gpu-pipeline") and lines[2].endswith(",yes")
-    with redirect_stdout(io.StringIO()):
+    out = io.StringIO()
+    with redirect_stdout(out):
         assert cli_main(["verify", "--size", "20", "-T", "4", "--team-size", "1", "--sweeps", "2",
                          "--depth", "3"]) == 0
         assert cli_main(["dist", "--dims", "12x10x32", "--layout", "1x1x2", "-T", "2",
                          "--team-size", "2", "--outer-steps", "2"]) == 0
+    # the device is checked against the reference package's own code (baseline/_ref), never itself
+    assert "/reference " in out.getvalue() and "(reference)" in out.getvalue()
+    assert out.getvalue().count("PASS (bitwise") == 2
+
+
+@pytest.mark.gpu
+def test_cli_compressed_and_float32_on_gpu():
+    """--storage compressed (R/bench.py:114,147-150,199-201; reference test_bench.py:81-92)
+    and --dtype float32, both verified against the reference package."""
+    from paper_0912_4506_b200.cli import cli_main
+    out = io.StringIO()
+    with redirect_stdout(out):
+        rc = cli_main(["bench", "--size", "16", "--variant", "pipeline", "--storage", "compressed",
+                       "--teams", "1", "--team-size", "2", "-T", "1", "--block", "16x8x8",
+                       "--sweeps", "3", "--reps", "1"])
+    assert rc == 0, out.getvalue()
+    row = out.getvalue().strip().split("\n")[1].split(",")
+    assert row[0] == "gpu-pipeline" and row[11] == "compressed" and row[-1] == "yes"
+    out = io.StringIO()
+    with redirect_stdout(out):
+        assert cli_main(["verify", "--size", "16", "--storage", "compressed", "--team-size", "2",
+                         "-T", "2", "--sweeps", "3"]) == 0
+        assert cli_main(["verify", "--size", "20", "--dtype", "float32", "-T", "4", "--team-size", "1",
+                         "--sweeps", "2"]) == 0
+        assert cli_main(["dist", "--dims", "12x10x32", "--layout", "1x1x2", "-T", "2", "--team-size", "2",
+                         "--outer-steps", "2", "--dtype", "float32"]) == 0
+    assert "gpu-compressed/reference" in out.getvalue()
+
+
+def test_reference_field_is_the_reference_code(O):
+    """The CLI's verification field comes from the reference package's own sweep
+    (baseline/_ref or --reference-path), bit-equal to the pinned oracle, fp32 included."""
+    import os
+    import numpy as np
+    from paper_0912_4506_b200 import GridDims
+    from paper_0912_4506_b200.cli import ReferenceUnavailable, _reference_field, build_parser
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not os.path.isdir(os.path.join(root, "baseline", "_ref", "stencilpipe")) and not os.path.isdir(REF):
+        pytest.skip("reference package not installed")
+    a = build_parser().parse_args(["verify", "--size", "9", "--pattern", "random", "--seed", "7"] +
+                                  ([] if os.path.isdir(os.path.join(root, "baseline", "_ref")) else
+                                   ["--reference-path", REF]))
+    d = GridDims(9, 8, 7)
+    ref64, src = _reference_field(a, d, None, 3, np.float64)
+    assert src == "reference"
+    g = O.CGrid(d.shape, O.BoxPattern("random", seed=7))
+    g.sweeps(3)
+    assert np.array_equal(ref64.view(np.uint64), g.interior().view(np.uint64))
+    ref32, _ = _reference_field(a, d, None, 3, np.float32)
+    g32 = O.CGrid(d.shape, O.BoxPattern("random", seed=7), dtype=np.float32)
+    g32.sweeps(3)
+    assert ref32.dtype == np.float32 and np.array_equal(ref32.view(np.uint32), g32.interior().view(np.uint32))
+    with pytest.raises(ReferenceUnavailable):
+        _import_reference_no_default(build_parser().parse_args(["verify"]))
+
+
+def _import_reference_no_default(args):
+    import builtins
+    real = builtins.__import__
+
+    def fake(name, *a, **k):
+        if name.startswith("stencilpipe"):
+            raise ImportError(name)
+        return real(name, *a, **k)
+    builtins.__import__ = fake
+    try:
+        from paper_0912_4506_b200.cli import _import_reference
+        _import_reference(args)
+    finally:
+        builtins.__import__ = real
