@@ -144,7 +144,9 @@ int sp_copy_out(const void* base, int dtype, const sp_layout* L, void* host, voi
  * sp_ipc_export: 64-byte handle of the device allocation holding ptr and
  * ptr's byte offset inside it.  sp_ipc_import (another process): map it into
  * the current device (peer access to the owner's GPU enabled on demand) and
- * return the address of the exported byte.  sp_ipc_close unmaps. */
+ * return the address of the exported byte.  sp_ipc_close unmaps.  Imports
+ * are refcounted per (device, handle): buffers exported from one allocation
+ * block share one mapping, closed with the last sp_ipc_close. */
 int sp_ipc_export(const void* ptr, unsigned char handle[64], int64_t* offset);
 int sp_ipc_import(const unsigned char handle[64], int64_t offset, void** ptr);
 int sp_ipc_close(void* ptr, int64_t offset);
@@ -173,7 +175,8 @@ int sp_probe_fp64(double* dadd_per_s, double* ms);
  * rows-per-thread / z-queue slots; a variant not built for a depth falls back
  * to variant 0; -1 = single-level sweeps on the K1 kernel) and z-chunk count
  * override (0 = automatic).  Returns the previous values encoded as
- * (variant+1)*1000 + chunks. */
+ * (variant+1)*1000 + chunks.  The setting is THREAD-LOCAL: it applies to the
+ * calling host thread's later launches only. */
 int sp_set_tuning(int variant, int chunks);
 
 /* Tuning hook (benchmarks only): work-unit schedule of the temporally blocked
@@ -182,7 +185,10 @@ int sp_set_tuning(int variant, int chunks);
  * share their halo rows through L2; 0: static round-robin.  strip = width in
  * tiles of the column strips units are ordered by (y-major inside a strip;
  * 0 = plain x-major rows).  Negative arguments keep the current value.
- * Returns the previous values encoded as dynamic*1000 + strip. */
+ * Returns the previous values encoded as dynamic*1000 + strip.  Thread-local
+ * like sp_set_tuning.  The dynamic schedule's unit counter is one per (device,
+ * stream): launches on a stream are serial and each leaves it at zero, and
+ * launches on different streams never share one. */
 int sp_set_schedule(int dynamic, int strip);
 
 /* Compressed single-array storage (R/grid.py:164-208; R/kernel.py:83-121):

@@ -13,7 +13,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
+#include <thread>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -57,10 +60,12 @@ namespace {
 
 using namespace spi;
 
-int g_chunks = 0;
-int g_use_k1 = 0;   // 1: single-level sweeps use the L1-streaming K1 kernel instead of K2(T=1)
-int g_dynamic = 1;  // K2 unit schedule: 1 = claimed in order from a device counter, 0 = round-robin
-int g_strip = 0;    // K2 unit order: tile-column strips this wide (0 = x-major rows)
+// Tuning overrides (benchmarks and tests only; sp_set_tuning / sp_set_schedule):
+// thread-local, so one host thread's experiments never change another's launches.
+thread_local int g_chunks = 0;
+thread_local int g_use_k1 = 0;   // 1: single-level sweeps use the L1-streaming K1 kernel instead of K2(T=1)
+thread_local int g_dynamic = 1;  // K2 unit schedule: 1 = claimed in order from a device counter, 0 = round-robin
+thread_local int g_strip = 0;    // K2 unit order: tile-column strips this wide (0 = x-major rows)
 
 
 struct DevInfo {
@@ -93,32 +98,44 @@ int check_layout(const sp_layout* L, int dtype) {
     return SP_OK;
 }
 
-// Dynamic-schedule unit counters: kCounters per device, zeroed once; each
-// K2 launch takes the next one (launches on different streams may overlap)
-// and the kernel leaves it at zero again.  Reuse needs kCounters launches in
-// flight at once.
-constexpr int kCounters = 1024;
+// Dynamic-schedule unit counters: one per (device, stream).  Launches on one
+// stream run one after another and every K2 launch leaves its counter at zero
+// again (the last CTA to overshoot re-arms it), so a stream's launches can
+// share one counter; launches on different streams -- which may overlap --
+// never do.  The per-thread default stream (handle cudaStreamPerThread) is a
+// different stream in every host thread, so its key includes the thread.
+// Counters come from device blocks of kCounterBlock, zeroed once, never freed.
+constexpr int kCounterBlock = 1024;
 
-int sched_counter(unsigned** out) {
+int sched_counter(cudaStream_t stream, unsigned** out) {
     static std::mutex mu;
-    static unsigned* base[64] = {};
-    static uint32_t next[64] = {};
+    static std::map<std::tuple<int, uintptr_t, std::thread::id>, unsigned*> slots;
+    static unsigned* block[64] = {};
+    static int used[64] = {};
     int dev = 0;
     SP_CUDA(cudaGetDevice(&dev));
     if (dev < 0 || dev >= 64) return fail(SP_ERR_DEVICE, "device ordinal %d out of range", dev);
+    const std::thread::id tid = stream == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id();
+    const auto key = std::make_tuple(dev, reinterpret_cast<uintptr_t>(stream), tid);
     std::lock_guard<std::mutex> lock(mu);
-    if (!base[dev]) {
-        unsigned* p = nullptr;
-        SP_CUDA(cudaMalloc(&p, kCounters * sizeof(unsigned)));
-        SP_CUDA(cudaMemset(p, 0, kCounters * sizeof(unsigned)));
-        base[dev] = p;
+    auto it = slots.find(key);
+    if (it != slots.end()) {
+        *out = it->second;
+        return SP_OK;
     }
-    *out = base[dev] + (next[dev]++ % kCounters);
+    if (!block[dev] || used[dev] == kCounterBlock) {
+        unsigned* p = nullptr;
+        SP_CUDA(cudaMalloc(&p, kCounterBlock * sizeof(unsigned)));
+        SP_CUDA(cudaMemset(p, 0, kCounterBlock * sizeof(unsigned)));
+        block[dev] = p;
+        used[dev] = 0;
+    }
+    *out = block[dev] + used[dev]++;
+    slots.emplace(key, *out);
     return SP_OK;
 }
 
-
-int g_variant_override = -1;
+thread_local int g_variant_override = -1;
 
 // Default variant per (dtype, T), from same-box B200 sweeps
 // (profiles/r01_tuning.md, "split barrier" table).
@@ -470,20 +487,52 @@ int sp_ipc_export(const void* ptr, unsigned char handle[64], int64_t* offset) {
     return SP_OK;
 }
 
+// Imported IPC mappings, refcounted by handle: the handle names a whole
+// cudaMalloc block, and two exported buffers (a neighbour's A and B) may come
+// from the same caching-allocator block -- the block is opened once per
+// process and closed with its last user.
+namespace {
+struct IpcMap {
+    void* base;
+    int refs;
+};
+std::mutex g_ipc_mu;
+std::map<std::pair<int, std::string>, IpcMap> g_ipc;
+std::map<void*, std::pair<int, std::string>> g_ipc_by_base;
+}  // namespace
+
 int sp_ipc_import(const unsigned char handle[64], int64_t offset, void** ptr) {
     if (!handle || !ptr) return fail(SP_ERR_ARG, "null argument");
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, handle, 64);
-    void* base = nullptr;
-    // mapped into the current device; peer access to the owner's device is enabled lazily
-    SP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
-    *ptr = (char*)base + offset;
+    int dev = 0;
+    SP_CUDA(cudaGetDevice(&dev));
+    const auto key = std::make_pair(dev, std::string(reinterpret_cast<const char*>(handle), 64));
+    std::lock_guard<std::mutex> lock(g_ipc_mu);
+    auto it = g_ipc.find(key);
+    if (it == g_ipc.end()) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, 64);
+        void* base = nullptr;
+        // mapped into the current device; peer access to the owner's device is enabled lazily
+        SP_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        it = g_ipc.emplace(key, IpcMap{base, 0}).first;
+        g_ipc_by_base[base] = key;
+    }
+    ++it->second.refs;
+    *ptr = (char*)it->second.base + offset;
     return SP_OK;
 }
 
 int sp_ipc_close(void* ptr, int64_t offset) {
     if (!ptr) return SP_OK;
-    SP_CUDA(cudaIpcCloseMemHandle((char*)ptr - offset));
+    void* base = (char*)ptr - offset;
+    std::lock_guard<std::mutex> lock(g_ipc_mu);
+    auto b = g_ipc_by_base.find(base);
+    if (b == g_ipc_by_base.end()) return fail(SP_ERR_ARG, "sp_ipc_close: %p is not an imported mapping", base);
+    auto it = g_ipc.find(b->second);
+    if (--it->second.refs > 0) return SP_OK;
+    g_ipc.erase(it);
+    g_ipc_by_base.erase(b);
+    SP_CUDA(cudaIpcCloseMemHandle(base));
     return SP_OK;
 }
 
@@ -735,7 +784,7 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     a.strip = g_strip;
     a.sched = nullptr;
     if ((g_dynamic || inplace) && cl == 1 && ls == 1) {   // in place: units must be claimed in order
-        rc = sched_counter(&a.sched);
+        rc = sched_counter((cudaStream_t)stream, &a.sched);
         if (rc) return rc;
     }
     a.zshift = 0;
