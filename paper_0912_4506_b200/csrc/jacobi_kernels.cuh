@@ -177,6 +177,18 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
     } while (!ok);
 }
 
+// remote arrive with the default semantics: the consumer's hand-back of a ring
+// slot to the CTA that fills it with st.async (a WAR release only: no data is
+// published).  This is the stage-release pattern of CUTLASS's cluster
+// pipelines (ClusterBarrier::arrive: plain mbarrier.arrive.shared::cluster,
+// waited on with a plain try_wait).  The cluster-scope release/acquire pair
+// the PTX model asks for compiles to MEMBAR.ALL.GPU + CCTL.IVALL per step and
+// costs the level-split kernels 25-28 % (measured: T=6 521 -> 419, T=8 410 ->
+// 298 GLUP/s), so the hand-back keeps the CUTLASS form.
+__device__ __forceinline__ void mbar_arrive_remote_cta(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
 // 16-byte (fp64) / 8-byte (fp32) asynchronous store into another CTA's shared
 // memory that completes `bytes` of transaction on that CTA's mbarrier
 template <typename R> struct StAsync;
@@ -511,9 +523,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         }
         mbar_expect_tx(&full[slot], kRingBytes);
         if (LS == 1 || first) tma_load_3d(ring + slot * RPLANE, &tmap, &full[slot], pc0, pc1, pc2);
-        // rank r-1 may fill this slot: release at cluster scope orders this CTA's
-        // reads of the slot before the other CTA's st.async overwrites it (WAR)
-        else mbar_arrive_remote(pv_empty + 8u * slot);
+        else mbar_arrive_remote_cta(pv_empty + 8u * slot);   // rank r-1 may fill this slot (see above)
         if (++pc2 == pc2_end) producer_unit();
     };
     if (threadIdx.x == 0) {
@@ -820,7 +830,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             if (LS > 1 && !last && st >= 2 * D) {
                 // level L0+D of plane q-D -> the next rank's ring, once it has freed the slot
                 const uint32_t s1 = gsent % RING_N;
-                mbar_wait_cluster(&empty[s1], (gsent / RING_N) & 1);   // acquire.cluster pairs it
+                mbar_wait(&empty[s1], (gsent / RING_N) & 1);
                 const uint32_t base = nx_ring + (uint32_t)((s1 * RPLANE + cy * WX + cx) * sizeof(R));
 #pragma unroll
                 for (int j = 0; j < PY; ++j)
