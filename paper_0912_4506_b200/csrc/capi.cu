@@ -145,7 +145,7 @@ int default_variant(int dtype, int T) {
             case 1: return 5;    // 16x2/3, ring 6
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
             case 3: return 21;   // 12x3/3, split, running output pointer
-            case 4: return 15;   // 8x4/3, split, running output pointer
+            case 4: return 34;   // 12x3/2, split, running output pointer, hoisted xy sums (+8 % over 15)
             case 5: return 27;   // 8x4, level 0 re-read from the ring (slots 4), split
             case 6: return 25;   // level split over two CTAs, 12x3/3 each (3 levels per CTA)
             case 8: return 23;   // level split over two CTAs, 8x4/3 each (4 levels per CTA)
@@ -155,7 +155,7 @@ int default_variant(int dtype, int T) {
     switch (T) {
         case 1: return 14;       // 16x2/3
         case 2: return 16;       // 8x8/2, two CTAs per SM, split
-        case 3: return 22;       // 12x6/2, running output pointer
+        case 3: return 37;       // 12x6/2, running output pointer, hoisted xy sums (+3.5 % over 22)
         case 4: return 8;        // 8x8/2, running output pointer
         case 5:
         case 6: return 11;       // 16x2/2, split
@@ -193,7 +193,18 @@ bool is_usable(int v) {
         case 24: return usable<R, T, 24>();
         case 25: return usable<R, T, 25>();
         case 26: return usable<R, T, 26>();
-        default: return usable<R, T, 27>();
+        case 27: return usable<R, T, 27>();
+        case 28: return usable<R, T, 28>();
+        case 29: return usable<R, T, 29>();
+        case 30: return usable<R, T, 30>();
+        case 31: return usable<R, T, 31>();
+        case 32: return usable<R, T, 32>();
+        case 33: return usable<R, T, 33>();
+        case 34: return usable<R, T, 34>();
+        case 35: return usable<R, T, 35>();
+        case 36: return usable<R, T, 36>();
+        case 37: return usable<R, T, 37>();
+        default: return usable<R, T, 38>();
     }
 }
 
@@ -555,7 +566,9 @@ int sp_describe_variant(int dtype, int T, char* buf, int buflen) {
                                      : "level 0 re-read from the ring, 2-slot queue above";
         snprintf(buf, (size_t)buflen,
                  "variant %d: %d warps x %d rows (64x%d footprint), %s, %d CTA/SM, %s step sync%s%s%s",
-                 v, k.by, k.py, k.by * k.py * k.cl, q, k.minb, k.split ? "split mbarrier" : "__syncthreads",
+                 v, k.by, k.py, k.by * k.py * k.cl,
+                 k.lag == 2 ? "lag-2 z-wavefront (independent level updates), 3-slot queues" : q, k.minb,
+                 k.lag == 2 ? "triple-buffered mbarrier" : k.split ? "split mbarrier" : "__syncthreads",
                  k.rstore ? ", running output pointer" : "",
                  k.ls > 1 ? (k.ls == 2 ? ", level split over a 2-CTA cluster" : ", level split over a 4-CTA cluster")
                           : "",
@@ -771,7 +784,8 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
         int64_t nreal = (nzb + len - 1) / len;
         int64_t units = tiles * nreal;
         double waves = (double)((units + slots - 1) / slots);
-        double cost = waves * (double)(len + 2 * T);
+        // steps per unit: chunk + 2T planes (+ T-1 drain steps for the lag-2 wavefront)
+        double cost = waves * (double)(len + (kVariants[variant].lag == 2 ? 3 * T - 1 : 2 * T));
         if (cost < best_cost * 0.999) { best_cost = cost; best_n = nch; }
     }
     if (g_chunks > 0) best_n = std::min<int64_t>(g_chunks, nzb);

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #ifndef SP_L2_PROMO
 #define SP_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
@@ -45,6 +46,8 @@ struct Variant {
     int zcap = 0;                    // > 0: z-chunks at most this many planes (L2 locality)
     int cl = 1;                      // > 1: y-cooperative thread-block clusters of this size
     int ls = 1;                      // 2: level-split pipeline over a cluster of two CTAs
+    int lag = 1;                     // 2: lag-2 z-wavefront (tb2_kernel, wave2.cuh)
+    int hoist = 0;                   // xy-sum placement in the step (see tb_kernel HOIST)
 };
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
@@ -79,8 +82,22 @@ constexpr Variant kVariants[] = {
     {8, 8, 2, 1, 8, 1, 1, 0, 1, 4},    // 26: 64x64 footprint, chain of four CTAs (T=8: 2 levels each)
     // slots 4: level 0 re-read from the ring into step-parity registers (no level-0 moves)
     {8, 4, 4, 1, 8, 0, 1},         // 27: fp64 T=5: 12 with slots 4
+    // lag-2 z-wavefront (tb2_kernel): the T level updates of a step are independent
+    {8, 4, 3, 1, 8, 1, 1, 0, 1, 1, 2},    // 28: 8 warps x 4 rows
+    {12, 3, 3, 1, 8, 1, 1, 0, 1, 1, 2},   // 29: 12 warps x 3 rows
+    {8, 8, 3, 1, 8, 1, 1, 128, 1, 1, 2},  // 30: 8 warps x 8 rows (fp32)
+    {16, 2, 3, 1, 8, 1, 1, 0, 1, 1, 2},   // 31: 16 warps x 2 rows
+    // hoisted xy sums (HOIST 3: level 1's before the TMA wait, every deeper
+    // level's right after the step barrier; same-box A/B +4-6 % fp64 T=3/4)
+    {12, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 3},   // 32: fp64 T=3: 21 hoisted
+    {8, 4, 3, 1, 8, 1, 1, 0, 1, 1, 1, 3},    // 33: fp64 T=4: 15 hoisted
+    {12, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3},   // 34: 20 hoisted
+    {8, 4, 2, 2, 8, 0, 1, 80, 1, 1, 1, 1},   // 35: 9 with level 1's sums before the TMA wait (slower)
+    {8, 8, 2, 1, 8, 1, 0, 128, 1, 1, 1, 3},  // 36: fp32: 8 hoisted
+    {12, 6, 2, 1, 8, 1, 0, 128, 1, 1, 1, 3}, // 37: fp32: 22 hoisted
+    {8, 8, 2, 1, 8, 1, 1, 128, 1, 1, 1, 3},  // 38: fp32: 8 hoisted, split barrier
 };
-constexpr int kNumVariants = 28;
+constexpr int kNumVariants = 39;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -95,6 +112,15 @@ constexpr bool compiled() {
     if (V >= 23 && V <= 25) return T == 4 || T == 6 || T == 8;
     if (V == 26) return T == 8;
     if (V == 27) return sizeof(R) == 8 && T >= 4 && T <= 5;
+    if (V == 28) return T >= 2 && T <= 4;
+    if (V == 29) return T >= 2 && T <= 4;
+    if (V == 30) return sizeof(R) == 4 && T >= 2 && T <= 4;
+    if (V == 31) return T >= 2 && T <= 6;
+    if (V == 32) return sizeof(R) == 8 && T == 3;
+    if (V == 33) return sizeof(R) == 8 && T >= 4 && T <= 5;
+    if (V == 34) return sizeof(R) == 8 && T >= 3 && T <= 4;
+    if (V == 35) return T == 2;
+    if (V >= 36 && V <= 38) return sizeof(R) == 4 && T >= 3 && T <= 4;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -110,6 +136,8 @@ constexpr bool usable() {
     constexpr Variant v = kVariants[V];
     if constexpr (!compiled<R, T, V>()) {
         return false;
+    } else if constexpr (v.lag == 2) {
+        return T >= 2 && sp::Plan2<R, T, v.by, v.py, v.minb, v.ring>::FITS;
     } else {
         // level split: each CTA holds T/ls levels; the footprint still carries the T halo
         return sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>::FITS &&
@@ -124,9 +152,15 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
     } else {
         constexpr Variant v = kVariants[V];
-        using Pl = sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>;
-        auto kern = sp::tb_kernel<R, T, v.by, v.py, v.slots, v.minb, v.ring, v.rstore, v.split, PEER, v.cl,
-                                  v.ls, INPL>;
+        static_assert(v.lag == 1 || (!PEER && !INPL), "lag-2 variants: two-grid passes only");
+        using Pl = std::conditional_t<v.lag == 2, sp::Plan2<R, T, v.by, v.py, v.minb, v.ring>,
+                                      sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>>;
+        auto kern = [] {
+            constexpr Variant w = kVariants[V];
+            if constexpr (w.lag == 2) return sp::tb2_kernel<R, T, w.by, w.py, w.minb, w.ring>;
+            else return sp::tb_kernel<R, T, w.by, w.py, w.slots, w.minb, w.ring, w.rstore, w.split, PEER, w.cl,
+                                      w.ls, INPL, w.hoist>;
+        }();
         const size_t smem = Pl::SMEM;
         // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
         static std::atomic<uint64_t> attr_set{0};   // bit d: set on device d
@@ -222,7 +256,18 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 24: return launch_tb_t<R, T, 24>(src, L, a, grid, s);
         case 25: return launch_tb_t<R, T, 25>(src, L, a, grid, s);
         case 26: return launch_tb_t<R, T, 26>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 27>(src, L, a, grid, s);
+        case 27: return launch_tb_t<R, T, 27>(src, L, a, grid, s);
+        case 28: return launch_tb_t<R, T, 28>(src, L, a, grid, s);
+        case 29: return launch_tb_t<R, T, 29>(src, L, a, grid, s);
+        case 30: return launch_tb_t<R, T, 30>(src, L, a, grid, s);
+        case 31: return launch_tb_t<R, T, 31>(src, L, a, grid, s);
+        case 32: return launch_tb_t<R, T, 32>(src, L, a, grid, s);
+        case 33: return launch_tb_t<R, T, 33>(src, L, a, grid, s);
+        case 34: return launch_tb_t<R, T, 34>(src, L, a, grid, s);
+        case 35: return launch_tb_t<R, T, 35>(src, L, a, grid, s);
+        case 36: return launch_tb_t<R, T, 36>(src, L, a, grid, s);
+        case 37: return launch_tb_t<R, T, 37>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 38>(src, L, a, grid, s);
     }
 }
 

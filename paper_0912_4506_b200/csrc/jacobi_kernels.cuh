@@ -402,7 +402,7 @@ struct Plan {
 // CTA keeps only D levels of z-queue in registers, so T=8 fits where one CTA
 // holding all eight levels spills.
 template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV,
-          bool PEER = false, int CL = 1, int LS = 1, bool INPL = false>
+          bool PEER = false, int CL = 1, int LS = 1, bool INPL = false, int HOIST = 0>
 __global__ void __launch_bounds__(32 * BY, MINB)
     tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     // SLOTS = 4: levels >= 1 as SLOTS = 2; level 0's v[p] is re-read from the
@@ -707,6 +707,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 __syncthreads();   // single buffers: all reads before any overwrite
             }
 
+            // HOIST bit 0: level 1's xy sums (level 0 of the previous plane, already
+            // in the ring) before waiting for this step's TMA plane
+            if constexpr (P::DB && (HOIST & 1)) xy_sums(1);
             mbar_wait(&full[slot], (gstep / RING_N) & 1);
             // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
             R Nt[QS == 2 ? D : 1][PY][PX];
@@ -738,7 +741,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             R out[PY][PX];  // level-D values of plane q-D
 #pragma unroll
             for (int t = 1; t <= D; ++t) {
-                if constexpr (P::DB) xy_sums(t);
+                if constexpr (P::DB) {
+                    if (t == 1 ? !(HOIST & 1) : !(HOIST & 2)) xy_sums(t);
+                }
                 const R(&mm)[PY][PX] = *([&]() -> const R(*)[PY][PX] {
                     if constexpr (QS == 1) return &mv;
                     else if constexpr (L0C) return t == 1 ? &M0[M0I] : &Q[F0][t - 1];
@@ -798,6 +803,14 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                         // ring slot last read in step k-1: plane k-2 (k-3 with SLOTS == 1,
                         // which re-reads v[p-1] from slot k-2 at the start of a step)
                         produce(QS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
+                    }
+                }
+                // HOIST bit 1: every deeper level's xy sums at once, right after step
+                // k-1's level planes are known complete (independent DADD chains)
+                if constexpr (P::DB && (HOIST & 2)) {
+                    if (t == 1) {
+#pragma unroll
+                        for (int tt = 2; tt <= D; ++tt) xy_sums(tt);
                     }
                 }
                 if (t < D) {
@@ -930,6 +943,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     // no CTA leaves while a neighbour may still read its planes or arrive on its barriers
     if constexpr (CL > 1 || LS > 1) cluster_sync_all();
 }
+
+#include "wave2.cuh"   // tb2_kernel: the lag-2 z-wavefront form of K2
 
 // ---- K1: single-level streaming sweep ---------------------------------------
 //

@@ -18,9 +18,11 @@ from dataclasses import dataclass
 from . import _native as N
 from .grid import GridDims, TwoGrid, _on
 
-# Levels fused per HBM pass when the config does not say (tuned on B200;
-# see DESIGN.md "Choice of T").
-DEFAULT_DEPTH = {N.SP_F64: 2, N.SP_F32: 4}
+# Levels fused per HBM pass when the config does not say: the depth with the
+# highest SUSTAINED throughput on B200 (C3 1024^3 fp64, 100 sweeps: T=2 646,
+# T=3 723, T=4 757 GLUP/s -- T=2 saturates HBM and runs into the board power
+# cap at ~1640 MHz, T=4 stays near 1900 MHz).
+DEFAULT_DEPTH = {N.SP_F64: 4, N.SP_F32: 4}
 MAX_DEPTH = 8
 
 

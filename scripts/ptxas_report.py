@@ -30,6 +30,6 @@ names = list(rows)
 dem = subprocess.run(["cu++filt"], input="\n".join(names), capture_output=True, text=True).stdout.split("\n")
 for n, d in zip(names, dem):
     d = d.replace("(int)", "").replace("(bool)", "")
-    if "tb_kernel" in d and flt in d:
+    if ("tb_kernel" in d or "tb2_kernel" in d) and flt in d:
         r = rows[n]
         print(f"{r.get('regs', '?'):>4} regs  spill {r.get('spill', (0, 0))}  {d.split('(')[0]}")
