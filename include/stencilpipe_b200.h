@@ -209,6 +209,13 @@ int sp_sweep_tb_inplace(void* buf, int dtype, const sp_layout* L, int T, const i
 int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int to_grid, void* stream);
 int64_t sp_ghost_shell_elems(int64_t nx, int64_t ny, int64_t nz);
 
+/* Strided 3-D box copy on the device (K6): nz x ny x nx elements from src
+ * (row pitch src_py, plane pitch src_pz, in elements) to dst (dst_py,
+ * dst_pz).  Packs and unpacks the halo slabs of multi-axis decompositions
+ * (the extended slabs of R/decomp.py:137-179) around NCCL send/recv. */
+int sp_copy_box(const void* src, void* dst, int dtype, int64_t nz, int64_t ny, int64_t nx, int64_t src_py,
+                int64_t src_pz, int64_t dst_py, int64_t dst_pz, void* stream);
+
 /* Scatter only the ghost face cells adjacent to the interior box [lo, hi)
  * (z, y, x): a face only where the box touches it (lo == 0 / hi == n on that
  * axis), within the box's extent on the other axes, edges and corners never.

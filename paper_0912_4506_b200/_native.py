@@ -37,7 +37,7 @@ EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "
            "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_sweep_tb_part_peer", "sp_run_sweeps",
            "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule", "sp_ipc_export",
            "sp_ipc_import", "sp_ipc_close", "sp_copy_in", "sp_copy_out", "sp_describe_variant",
-           "sp_sweep_tb_inplace", "sp_ghost_shell", "sp_ghost_shell_elems", "sp_ghost_shell_region")
+           "sp_sweep_tb_inplace", "sp_ghost_shell", "sp_ghost_shell_elems", "sp_ghost_shell_region", "sp_copy_box")
 
 
 class NativeUnavailable(RuntimeError):
@@ -161,6 +161,7 @@ def load_library():
                                           ctypes.c_int64, ctypes.c_int, vp, ctypes.c_int64, vp]
         L.sp_ghost_shell.argtypes = [vp, ctypes.c_int, P(Layout), vp, ctypes.c_int, vp]
         L.sp_ghost_shell_region.argtypes = [vp, ctypes.c_int, P(Layout), vp, i64p, i64p, vp]
+        L.sp_copy_box.argtypes = [vp, vp, ctypes.c_int] + [ctypes.c_int64] * 7 + [vp]
         L.sp_ghost_shell_elems.restype = ctypes.c_int64
         L.sp_ghost_shell_elems.argtypes = [ctypes.c_int64] * 3
     if hasattr(L, "sp_describe_variant") or not override:

@@ -683,6 +683,17 @@ int sp_ghost_shell(void* base, int dtype, const sp_layout* L, void* shell, int t
     return ghost_shell(base, dtype, L, shell, to_grid, nullptr, nullptr, stream);
 }
 
+int sp_copy_box(const void* src, void* dst, int dtype, int64_t nz, int64_t ny, int64_t nx, int64_t src_py,
+                int64_t src_pz, int64_t dst_py, int64_t dst_pz, void* stream) {
+    if (!src || !dst) return fail(SP_ERR_ARG, "null argument");
+    if (elem_size(dtype) == 0) return fail(SP_ERR_ARG, "unknown dtype %d", dtype);
+    if (nz < 0 || ny < 0 || nx < 0 || src_py < nx || dst_py < nx || src_pz < src_py * ny || dst_pz < dst_py * ny)
+        return fail(SP_ERR_ARG, "inconsistent box copy extents/pitches");
+    if (nz == 0 || ny == 0 || nx == 0) return SP_OK;
+    sp::RowCopy c{nz, ny, nx, src_py, src_pz, dst_py, dst_pz};
+    return row_copy_dt(dtype, src, dst, nullptr, c, (cudaStream_t)stream);
+}
+
 int sp_ghost_shell_region(void* base, int dtype, const sp_layout* L, const void* shell, const int64_t lo[3],
                           const int64_t hi[3], void* stream) {
     if (!lo || !hi) return fail(SP_ERR_ARG, "null region");

@@ -182,19 +182,34 @@ def build_halo_plan(halo: int):
     return plan
 
 
+def box_view(buf, lay):
+    """The ghosted box of layout ``lay`` as a strided (z, y, x) view of the flat ``buf``."""
+    shape = (lay.nz + 2 * lay.gz, lay.ny + 2 * lay.gy, lay.nx + 2 * lay.gx)
+    return buf.as_strided(shape, (lay.pz, lay.py, 1), lay.origin - lay.gz * lay.pz - lay.gy * lay.py - lay.gx)
+
+
+def slab_box(lay, axis: int, ext, rng):
+    """(start element, (nz, ny, nx)) of the box over logical range ``rng`` on
+    ``axis`` and the interior (+ ext) on the tangential axes, in layout ``lay``."""
+    n = (lay.nz, lay.ny, lay.nx)
+    lo, ext_n = [], []
+    for d in range(3):
+        if d == axis:
+            a, b = rng
+        else:
+            a, b = -ext[d][0], n[d] + ext[d][1]
+        lo.append(a)
+        ext_n.append(b - a)
+    start = lay.origin + lo[0] * lay.pz + lo[1] * lay.py + lo[2]
+    return start, tuple(ext_n)
+
+
 def _slab(grid: TwoGrid, axis: int, ext, rng) -> "torch.Tensor":
     """View of ``grid.current`` over logical range ``rng`` on ``axis`` and the
     interior (+ ext) on the tangential axes."""
-    g = (grid.gz, grid.gxy, grid.gxy)
-    n = grid.dims.shape
-    sl = []
-    for d in range(3):
-        if d == axis:
-            lo, hi = rng
-        else:
-            lo, hi = -ext[d][0], n[d] + ext[d][1]
-        sl.append(slice(lo + g[d], hi + g[d]))
-    return grid.current[tuple(sl)]
+    lay = grid.layout
+    start, shape = slab_box(lay, axis, ext, rng)
+    return grid.current_buffer().as_strided(shape, (lay.pz, lay.py, 1), start)
 
 
 def exchange_halos_local(grids, decomp: Decomposition, h: int, order=("x", "y", "z")) -> None:

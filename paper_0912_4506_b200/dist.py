@@ -1,8 +1,11 @@
-"""Multi-process z-slab runner: one process per GPU, halos over torch.distributed.
+"""Multi-process domain-decomposed runner: one process per GPU, halos over torch.distributed.
 
 Mirrors the reference's distributed engine (exchange_halos + outer_step,
-R/decomp.py:149-237, R/transport.py as the message layer) for layouts
-(1, 1, P), with the halo exchange moved onto NCCL point-to-point
+R/decomp.py:149-237, R/transport.py as the message layer).  Any Cartesian
+layout (px, py, pz) runs the reference's extended-slab exchange x -> y -> z
+with device pack/unpack (K6, sp_copy_box) around NCCL send/recv, then the
+passes on the extended level domains.  For z-slab layouts (1, 1, P) -- the
+8-GPU configuration -- the exchange is moved onto NCCL point-to-point
 (``batch_isend_irecv`` of h contiguous padded z-planes, straight from and
 into the grid buffers) and OVERLAPPED with compute:
 
@@ -38,7 +41,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from .decomp import DecompositionError, decompose, face_flags, plane_spans
+from .decomp import (DecompositionError, _slab, build_halo_plan, decompose, face_flags, plane_spans,
+                     slab_box)
 from .grid import GridDims
 from .pipeline import DEFAULT_DEPTH, MAX_DEPTH
 
@@ -65,6 +69,32 @@ class CudaEngine:
     def sync(self, grid):
         import torch
         torch.cuda.current_stream(grid.device).synchronize()
+
+    def pack(self, grid, axis, ext, rng):
+        """The halo slab (R/decomp.py:137-179 geometry) of the current state as a
+        dense device buffer (K6 box copy, sp_copy_box)."""
+        import torch
+        from . import _native as N
+        lay = grid.layout
+        start, shape = slab_box(lay, axis, ext, rng)
+        buf = grid.current_buffer()
+        out = torch.empty(shape, dtype=buf.dtype, device=buf.device)
+        es = buf.element_size()
+        N.check(N.lib().sp_copy_box(ctypes_ptr(buf.data_ptr() + start * es), ctypes_ptr(out.data_ptr()),
+                                    grid.sp_dtype, *shape, lay.py, lay.pz, shape[2], shape[1] * shape[2],
+                                    grid.stream()))
+        return out
+
+    def unpack(self, grid, axis, ext, rng, data):
+        """A received dense slab into the current state's ghost layers (K6)."""
+        from . import _native as N
+        lay = grid.layout
+        start, shape = slab_box(lay, axis, ext, rng)
+        buf = grid.current_buffer()
+        es = buf.element_size()
+        N.check(N.lib().sp_copy_box(ctypes_ptr(data.data_ptr()), ctypes_ptr(buf.data_ptr() + start * es),
+                                    grid.sp_dtype, *shape, shape[2], shape[1] * shape[2], lay.py, lay.pz,
+                                    grid.stream()))
 
     def share(self, grid):
         """CUDA IPC handles of both grids (picklable)."""
@@ -97,6 +127,11 @@ class CudaEngine:
             N.check(N.lib().sp_ipc_close(b.ptr, b.offset))
 
 
+def ctypes_ptr(p: int):
+    import ctypes
+    return ctypes.c_void_p(p)
+
+
 class PeerBuffer:
     """A neighbour's grid allocation mapped into this process (CUDA IPC)."""
 
@@ -113,14 +148,19 @@ class SlabRunner:
 
     def __init__(self, global_dims: GridDims, pattern, h: int, dtype=np.float64,
                  depth: int | None = None, device=None, engine=None, overlap: bool = True,
-                 group=None, transport: str = "nccl"):
+                 group=None, transport: str = "nccl", layout=None, order=("x", "y", "z")):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.h = h
-        self.decomp = decompose(global_dims, self.world, (1, 1, self.world), h)
+        # (px, py, pz): z-slabs by default; any Cartesian layout runs the
+        # reference's extended-slab exchange x -> y -> z (R/decomp.py:125-179)
+        self.layout = tuple(layout) if layout is not None else (1, 1, self.world)
+        self.multi_axis = tuple(self.layout[:2]) != (1, 1)
+        self.order = tuple(order)
+        self.decomp = decompose(global_dims, self.world, self.layout, h)
         self.engine = engine or CudaEngine()
         self.grid = self.engine.make_grid(self.decomp, self.rank, pattern, dtype, device)
         self.depth = depth or self.engine.default_depth(self.grid)
@@ -128,14 +168,16 @@ class SlabRunner:
         self.lo_nb = self.decomp.neighbor(self.rank, 0, high=False)
         self.hi_nb = self.decomp.neighbor(self.rank, 0, high=True)
         nz = self.grid.dims.nz
-        # overlap needs one pass per outer step and a non-empty interior slab
-        self.overlap = overlap and h <= min(self.depth, MAX_DEPTH) and nz > 2 * h
+        # overlap needs one pass per outer step and a non-empty interior slab (z-slabs)
+        self.overlap = overlap and not self.multi_axis and h <= min(self.depth, MAX_DEPTH) and nz > 2 * h
         self._pending = []
         self._primed = False
         self.messages = 0
         self.bytes_sent = 0
         if transport not in ("nccl", "p2p"):
             raise DecompositionError(f"unknown halo transport {transport!r}")
+        if transport == "p2p" and self.multi_axis:
+            raise DecompositionError("the fused p2p transport serves z-slab layouts (1, 1, P) only")
         self.transport = transport
         if transport == "p2p":
             if not self.overlap:
@@ -259,8 +301,49 @@ class SlabRunner:
 
     def exchange(self):
         """Blocking exchange of the current state's halos (R/decomp.py:149-179)."""
+        if self.multi_axis:
+            self._exchange_phases()
+            return
         self._post(self.grid.current_buffer())
         self._wait()
+
+    def _exchange_phases(self):
+        """Multi-axis layouts: the phases in ``order`` one after another, each
+        slab carrying the ghost extensions of the canonically earlier axes
+        (build_halo_plan), so x -> y -> z delivers edges and corners
+        transitively like the reference (test_decomp.py:195-204).  Slabs are
+        packed into dense buffers on the device (sp_copy_box), moved by NCCL
+        send/recv, and unpacked into the ghost layers; a gloo group stages them
+        through host memory."""
+        import torch
+        dist, g, h = self.dist, self.grid, self.h
+        plan = build_halo_plan(h)
+        stage = dist.get_backend(self.group) != "nccl" and g.current_buffer().is_cuda
+        for name in self.order:
+            axis, ext = plan[name]
+            n = g.dims.shape[axis]
+            ops, pending = [], []
+            for high in (False, True):
+                nb = self.decomp.neighbor(self.rank, axis, high=high)
+                if nb is None:
+                    continue
+                sbuf = self.engine.pack(g, axis, ext, (n - h, n) if high else (0, h))
+                if stage:
+                    self.engine.sync(g)
+                    sbuf = sbuf.cpu()
+                rbuf = torch.empty_like(sbuf)
+                ops.append(dist.P2POp(dist.isend, sbuf, self._global_rank(nb), self.group))
+                ops.append(dist.P2POp(dist.irecv, rbuf, self._global_rank(nb), self.group))
+                pending.append((rbuf, (n, n + h) if high else (-h, 0), sbuf))
+                self.bytes_sent += sbuf.numel() * sbuf.element_size()
+            if ops:
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+                self.messages += len(ops) // 2
+            for rbuf, rng, _ in pending:
+                if stage:
+                    rbuf = rbuf.to(g.current_buffer().device)
+                self.engine.unpack(g, axis, ext, rng, rbuf)
 
     # -- compute -------------------------------------------------------------
 
@@ -338,11 +421,6 @@ class SlabRunner:
             sl = tuple(slice(a, b) for a, b in self.decomp.ranges(r))
             full[sl] = f
         return full
-
-
-def check_layout(layout):
-    if tuple(layout[:2]) != (1, 1):
-        raise DecompositionError("SlabRunner decomposes in z only: layout (1, 1, P)")
 
 
 def emulate_peer_slabs(global_dims: GridDims, pattern, ranks: int, h: int, levels, dtype=np.float64,

@@ -19,12 +19,12 @@ from paper_0912_4506_b200 import _native as N
 
 
 class HostGrid:
-    def __init__(self, dims, pattern: "O.BoxPattern", dtype, gz):
+    def __init__(self, dims, pattern: "O.BoxPattern", dtype, gz, gxy=1):
         L = N.load_library()
         lay = N.Layout()
         n = ctypes.c_int64()
         self.sp_dtype = N.SP_F64 if dtype == np.float64 else N.SP_F32
-        N.check(L.sp_layout_make(dims.nx, dims.ny, dims.nz, 1, 1, gz, self.sp_dtype,
+        N.check(L.sp_layout_make(dims.nx, dims.ny, dims.nz, gxy, gxy, gz, self.sp_dtype,
                                  ctypes.byref(lay), ctypes.byref(n)))
         self.layout = lay
         self.dims = dims
@@ -93,7 +93,16 @@ class HostEngine:
 
     def make_grid(self, decomp, rank, pattern, dtype, device):
         origin = tuple(r[0] for r in decomp.ranges(rank))
-        return HostGrid(decomp.local_dims(rank), self.base.shifted(origin), dtype, decomp.halo)
+        gxy = 1 if tuple(decomp.layout[:2]) == (1, 1) else decomp.halo
+        return HostGrid(decomp.local_dims(rank), self.base.shifted(origin), dtype, decomp.halo, gxy)
+
+    def pack(self, g, axis, ext, rng):
+        from paper_0912_4506_b200.decomp import _slab
+        return _slab(g, axis, ext, rng).contiguous().clone()
+
+    def unpack(self, g, axis, ext, rng, data):
+        from paper_0912_4506_b200.decomp import _slab
+        _slab(g, axis, ext, rng).copy_(data)
 
     def default_depth(self, grid):
         return 4
