@@ -147,8 +147,8 @@ int default_variant(int dtype, int T) {
             case 3: return 21;   // 12x3/3, split, running output pointer
             case 4: return 34;   // 12x3/2, split, running output pointer, hoisted xy sums (+8 % over 15)
             case 5: return 27;   // 8x4, level 0 re-read from the ring (slots 4), split
-            case 6: return 25;   // level split over two CTAs, 12x3/3 each (3 levels per CTA)
-            case 8: return 23;   // level split over two CTAs, 8x4/3 each (4 levels per CTA)
+            case 6: return 40;   // level split over two CTAs, 12x3/2 hoisted each (3 levels per CTA)
+            case 8: return 40;   // level split over two CTAs, 12x3/2 hoisted each (4 levels per CTA)
             default: return 12;  // 8x4/2, split
         }
     }
@@ -204,7 +204,10 @@ bool is_usable(int v) {
         case 35: return usable<R, T, 35>();
         case 36: return usable<R, T, 36>();
         case 37: return usable<R, T, 37>();
-        default: return usable<R, T, 38>();
+        case 38: return usable<R, T, 38>();
+        case 39: return usable<R, T, 39>();
+        case 40: return usable<R, T, 40>();
+        default: return usable<R, T, 41>();
     }
 }
 

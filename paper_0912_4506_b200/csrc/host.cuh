@@ -89,15 +89,20 @@ constexpr Variant kVariants[] = {
     {16, 2, 3, 1, 8, 1, 1, 0, 1, 1, 2},   // 31: 16 warps x 2 rows
     // hoisted xy sums (HOIST 3: level 1's before the TMA wait, every deeper
     // level's right after the step barrier; same-box A/B +4-6 % fp64 T=3/4)
-    {12, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 3},   // 32: fp64 T=3: 21 hoisted
+    {12, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 1},   // 32: 21 with level 1's sums hoisted (3 slots + HOIST 3
+                                             //     puts the queues in local memory: 10x slower)
     {8, 4, 3, 1, 8, 1, 1, 0, 1, 1, 1, 3},    // 33: fp64 T=4: 15 hoisted
     {12, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3},   // 34: 20 hoisted
     {8, 4, 2, 2, 8, 0, 1, 80, 1, 1, 1, 1},   // 35: 9 with level 1's sums before the TMA wait (slower)
     {8, 8, 2, 1, 8, 1, 0, 128, 1, 1, 1, 3},  // 36: fp32: 8 hoisted
     {12, 6, 2, 1, 8, 1, 0, 128, 1, 1, 1, 3}, // 37: fp32: 22 hoisted
     {8, 8, 2, 1, 8, 1, 1, 128, 1, 1, 1, 3},  // 38: fp32: 8 hoisted, split barrier
+    // level-split pipelines with hoisted xy sums
+    {8, 4, 3, 1, 8, 1, 1, 0, 1, 2, 1, 1},    // 39: 23, level 1's sums hoisted
+    {12, 3, 2, 1, 8, 1, 1, 0, 1, 2, 1, 3},   // 40: fp64 T=6, 8: 34 per CTA (12x3/2 hoisted), two-CTA chain
+    {12, 3, 3, 1, 8, 1, 1, 0, 1, 2, 1, 1},   // 41: 25, level 1's sums hoisted
 };
-constexpr int kNumVariants = 39;
+constexpr int kNumVariants = 42;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -121,6 +126,7 @@ constexpr bool compiled() {
     if (V == 34) return sizeof(R) == 8 && T >= 3 && T <= 4;
     if (V == 35) return T == 2;
     if (V >= 36 && V <= 38) return sizeof(R) == 4 && T >= 3 && T <= 4;
+    if (V >= 39 && V <= 41) return T == 4 || T == 6 || T == 8;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -267,7 +273,10 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 35: return launch_tb_t<R, T, 35>(src, L, a, grid, s);
         case 36: return launch_tb_t<R, T, 36>(src, L, a, grid, s);
         case 37: return launch_tb_t<R, T, 37>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 38>(src, L, a, grid, s);
+        case 38: return launch_tb_t<R, T, 38>(src, L, a, grid, s);
+        case 39: return launch_tb_t<R, T, 39>(src, L, a, grid, s);
+        case 40: return launch_tb_t<R, T, 40>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 41>(src, L, a, grid, s);
     }
 }
 

@@ -900,30 +900,37 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         };
         // warp-uniform: the whole warp is inside every level's x/y domain
         const bool fast_xy = fastm == (1u << D) - 1u;
-        // planes q-t of every level inside its z domain
-        auto zin_all = [&](int st) {
-            const int q = w.zc0 - Te + st;
-            return q - 1 < a.hi[0] + a.ehi[0] * (T - L0 - 1) && q - D >= a.lo[0];
+        // planes q-t of every level inside its z domain <=> st in [fs, fe) below
+        // Steps [fs, fe) are FAST for the whole warp (zin_all is an interval in
+        // st); they run as a branch-free loop unrolled by the z-queue period, the
+        // rest step by step with a per-step FAST/SLOW choice.
+        constexpr int PER = (QS == 1 || L0C) ? 2 : (QS == 3 ? 3 : 1);
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, PER >= 2 ? 1 : 0>;
+        using I2 = std::integral_constant<int, PER >= 3 ? 2 : 0>;
+        auto one = [&](auto fast, int st) {
+            const int ph = PER == 1 ? 0 : st % PER;
+            if (ph == 0) step(I0{}, fast, st);
+            else if (PER >= 2 && ph == 1) step(I1{}, fast, st);
+            else if (PER >= 3) step(I2{}, fast, st);
         };
-        auto run = [&](auto phase, int st) {
-            if (fast_xy && zin_all(st)) step(phase, std::true_type{}, st);
-            else step(phase, std::false_type{}, st);
-        };
-
-        if constexpr (QS == 1 || L0C) {
-            for (int st = 0; st < nsteps; st += 2) {
-                run(std::integral_constant<int, 0>{}, st);
-                if (st + 1 < nsteps) run(std::integral_constant<int, 1>{}, st + 1);
-            }
-        } else if constexpr (QS == 3) {
-            for (int st = 0; st < nsteps; st += 3) {
-                run(std::integral_constant<int, 0>{}, st);
-                if (st + 1 < nsteps) run(std::integral_constant<int, 1>{}, st + 1);
-                if (st + 2 < nsteps) run(std::integral_constant<int, 2>{}, st + 2);
-            }
-        } else {
-            for (int st = 0; st < nsteps; ++st) run(std::integral_constant<int, 0>{}, st);
+        int fs = nsteps, fe = nsteps;
+        if (fast_xy) {
+            const int q0 = w.zc0 - Te;    // q of step 0
+            fs = max(0, a.lo[0] + D - q0);
+            fe = min(nsteps, a.hi[0] + a.ehi[0] * (T - L0 - 1) + 1 - q0);
+            if (fe <= fs) fs = fe = nsteps;
         }
+        int st = 0;
+        for (; st < fs; ++st) one(std::false_type{}, st);
+        for (; st < fe && st % PER != 0; ++st) one(std::true_type{}, st);
+        for (; st + PER <= fe; st += PER) {
+            step(I0{}, std::true_type{}, st);
+            if constexpr (PER >= 2) step(I1{}, std::true_type{}, st + 1);
+            if constexpr (PER >= 3) step(I2{}, std::true_type{}, st + 2);
+        }
+        for (; st < fe; ++st) one(std::true_type{}, st);
+        for (; st < nsteps; ++st) one(std::false_type{}, st);
         if constexpr (INPL) {
             if (threadIdx.x == 0) {
                 // this thread consumed the unit's last plane: all its global reads (TMA) are done
