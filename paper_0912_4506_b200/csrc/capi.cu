@@ -207,7 +207,10 @@ bool is_usable(int v) {
         case 38: return usable<R, T, 38>();
         case 39: return usable<R, T, 39>();
         case 40: return usable<R, T, 40>();
-        default: return usable<R, T, 41>();
+        case 41: return usable<R, T, 41>();
+        case 42: return usable<R, T, 42>();
+        case 43: return usable<R, T, 43>();
+        default: return usable<R, T, 44>();
     }
 }
 

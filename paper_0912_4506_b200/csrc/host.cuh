@@ -101,8 +101,12 @@ constexpr Variant kVariants[] = {
     {8, 4, 3, 1, 8, 1, 1, 0, 1, 2, 1, 1},    // 39: 23, level 1's sums hoisted
     {12, 3, 2, 1, 8, 1, 1, 0, 1, 2, 1, 3},   // 40: fp64 T=6, 8: 34 per CTA (12x3/2 hoisted), two-CTA chain
     {12, 3, 3, 1, 8, 1, 1, 0, 1, 2, 1, 1},   // 41: 25, level 1's sums hoisted
+    // 10-11 warps x 3 rows: room (<= 200 registers) for the 3-slot queue at T=4 (no moves)
+    {10, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 1},   // 42
+    {11, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 1},   // 43
+    {10, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 0},   // 44
 };
-constexpr int kNumVariants = 42;
+constexpr int kNumVariants = 45;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -127,6 +131,7 @@ constexpr bool compiled() {
     if (V == 35) return T == 2;
     if (V >= 36 && V <= 38) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V >= 39 && V <= 41) return T == 4 || T == 6 || T == 8;
+    if (V >= 42 && V <= 44) return sizeof(R) == 8 && T >= 3 && T <= 5;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -276,7 +281,10 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 38: return launch_tb_t<R, T, 38>(src, L, a, grid, s);
         case 39: return launch_tb_t<R, T, 39>(src, L, a, grid, s);
         case 40: return launch_tb_t<R, T, 40>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 41>(src, L, a, grid, s);
+        case 41: return launch_tb_t<R, T, 41>(src, L, a, grid, s);
+        case 42: return launch_tb_t<R, T, 42>(src, L, a, grid, s);
+        case 43: return launch_tb_t<R, T, 43>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 44>(src, L, a, grid, s);
     }
 }
 

@@ -628,7 +628,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         // the warp is inside every level's domain this step, so the update is
         // straight-line; otherwise cells outside D_t keep their previous-level
         // value (Dirichlet walls, rank faces) through a per-cell select.
-        auto step = [&](auto phase, auto fast, int st) {
+        // always inlined: a step that became a call would take the register
+        // queues by reference, i.e. through local memory
+        auto step = [&](auto phase, auto fast, int st) __attribute__((always_inline)) {
             constexpr int PH = decltype(phase)::value;
             constexpr int F0 = QS == 3 ? PH : 0;                               // v[p-1]
             constexpr int F1 = QS == 3 ? (PH + 1) % 3 : (QS == 1 ? PH : 1);    // v[p]
@@ -652,7 +654,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     M0[C0][j][1] = r.y;
                 }
             }
-            auto qcur = [&](int t) -> const R(&)[PY][PX] {   // level t's v[p]
+            auto qcur = [&](int t) __attribute__((always_inline)) -> const R(&)[PY][PX] {   // level t's v[p]
                 if constexpr (L0C) return t == 0 ? M0[C0] : Q[F1][t];
                 else return Q[F1][t];
             };
@@ -661,7 +663,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             // the previous step (ring slot pslot / level buffer prv; own and
             // lane-neighbour cells from the registers of Q[F1]).
             R s[D][PY][PX];
-            auto xy_sums = [&](int t) {
+            auto xy_sums = [&](int t) __attribute__((always_inline)) {
                 const R* Pl = (t == 1) ? ring + pslot * RPLANE + HR * WX
                                        : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
                 const R(&v)[PY][PX] = qcur(t - 1);
@@ -713,7 +715,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             mbar_wait(&full[slot], (gstep / RING_N) & 1);
             // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
             R Nt[QS == 2 ? D : 1][PY][PX];
-            auto newv = [&](int t) -> R(&)[PY][PX] {
+            auto newv = [&](int t) __attribute__((always_inline)) -> R(&)[PY][PX] {
                 if constexpr (QS != 2) return Q[F2][t];
                 else return Nt[t];
             };
@@ -908,7 +910,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         using I0 = std::integral_constant<int, 0>;
         using I1 = std::integral_constant<int, PER >= 2 ? 1 : 0>;
         using I2 = std::integral_constant<int, PER >= 3 ? 2 : 0>;
-        auto one = [&](auto fast, int st) {
+        auto one = [&](auto fast, int st) __attribute__((always_inline)) {
             const int ph = PER == 1 ? 0 : st % PER;
             if (ph == 0) step(I0{}, fast, st);
             else if (PER >= 2 && ph == 1) step(I1{}, fast, st);
