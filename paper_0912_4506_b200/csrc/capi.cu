@@ -252,9 +252,7 @@ int launch_tb_kind(int kind, int T, int v, const void* src, const sp_layout* L, 
 }
 
 int inplace_variant_rt(int dtype, int T) {
-    static const int f64[9] = {0, 5, 13, 13, 12, 12, 12, 12, 12};
-    static const int f32[9] = {0, 14, 4, 22, 8, 11, 11, 2, 2};
-    return (dtype == SP_F64 ? f64 : f32)[T];
+    return (dtype == SP_F64 ? kInplaceF64 : kInplaceF32)[T];
 }
 
 struct PeerArgs {

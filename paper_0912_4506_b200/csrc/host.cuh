@@ -299,13 +299,22 @@ constexpr int kPeerVariant = 0;
 // T=3 12x3, T=4 8x4/3, fp32 T=2) would spill.  fp64 T=2,3: 8x4/3 with one
 // __syncthreads per step (measured: 562 / 524-538 GLUP/s against 457 / 512
 // for 16x2/3 and 8x4/2 with the split barrier; at T=4 it spills: 355 vs 507).
+#ifndef SP_INPL64_T2
+#define SP_INPL64_T2 13
+#endif
+#ifndef SP_INPL64_T3
+#define SP_INPL64_T3 13
+#endif
+#ifndef SP_INPL64_T4
+#define SP_INPL64_T4 12
+#endif
+constexpr int kInplaceF64[9] = {0, 5, SP_INPL64_T2, SP_INPL64_T3, SP_INPL64_T4, 12, 12, 12, 12};
+constexpr int kInplaceF32[9] = {0, 14, 4, 22, 8, 11, 11, 2, 2};
+
 template <typename R, int T>
 constexpr int inplace_variant() {
-    if constexpr (sizeof(R) == 8) {
-        return T == 1 ? 5 : T <= 3 ? 13 : 12;
-    } else {
-        return T == 1 ? 14 : T == 2 ? 4 : T == 3 ? 22 : T == 4 ? 8 : T <= 6 ? 11 : 2;
-    }
+    if constexpr (sizeof(R) == 8) return kInplaceF64[T];
+    else return kInplaceF32[T];
 }
 
 // One entry per (dtype, T), explicitly instantiated in its own unit:
