@@ -389,7 +389,9 @@ def main():
     if args.variant:
         lib.sp_set_tuning(args.variant, 0)
     sp_dtype = N.SP_F64 if dt == "f64" else N.SP_F32
-    T = args.depth or (C5_DEPTH if args.workload.startswith("c5") else DEFAULT_DEPTH[sp_dtype])
+    from paper_0912_4506_b200.pipeline import DEFAULT_DEPTH_INPLACE
+    T = args.depth or (C5_DEPTH if args.workload.startswith("c5") else
+                       DEFAULT_DEPTH_INPLACE[sp_dtype] if args.storage == "compressed" else DEFAULT_DEPTH[sp_dtype])
     if strong:
         gshape = shape
     else:

@@ -23,6 +23,9 @@ from .grid import GridDims, TwoGrid, _on
 # T=3 723, T=4 757 GLUP/s -- T=2 saturates HBM and runs into the board power
 # cap at ~1640 MHz, T=4 stays near 1900 MHz).
 DEFAULT_DEPTH = {N.SP_F64: 4, N.SP_F32: 4}
+# In-place passes (compressed storage) run fastest at T=3 (C3 1024^3, chunk 64: T=2 566, T=3 603,
+# T=4 517 GLUP/s; the per-unit chunk wait makes deeper in-place passes spill).
+DEFAULT_DEPTH_INPLACE = {N.SP_F64: 3, N.SP_F32: 4}
 MAX_DEPTH = 8
 
 
@@ -193,6 +196,8 @@ def run_pass(grid: TwoGrid, T: int, lo, hi, e_lo=(0, 0, 0), e_hi=(0, 0, 0),
 
 def sweeps(grid: TwoGrid, levels: int, depth: int | None = None) -> None:
     """``levels`` full-interior levels as passes of ``depth`` (one call, no host sync)."""
+    if getattr(grid, "storage", None) == "compressed":
+        depth = depth or DEFAULT_DEPTH_INPLACE[grid.sp_dtype]
     depth = depth or DEFAULT_DEPTH[grid.sp_dtype]
     if not 1 <= depth <= MAX_DEPTH:
         raise ScheduleError(f"device pass depth must be in 1..{MAX_DEPTH}")
