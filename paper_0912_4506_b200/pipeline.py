@@ -229,7 +229,7 @@ def run_node_sweeps(grid: TwoGrid, cfg: PipelineConfig, sweeps_: int,
         raise ValueError("config expects two-grid storage")
     U = cfg.levels_per_sweep
     check_schedule(grid.dims, cfg, level_domains)
-    depth = cfg.depth or DEFAULT_DEPTH[grid.sp_dtype]
+    depth = cfg.depth or (DEFAULT_DEPTH_INPLACE if compressed else DEFAULT_DEPTH)[grid.sp_dtype]
     if compressed and level_domains is not None:
         raise ScheduleError("compressed storage supports interior domains only")   # R/pipeline.py:312-313
     if compressed and grid.reference_slack:
