@@ -147,8 +147,8 @@ int default_variant(int dtype, int T) {
             case 3: return 21;   // 12x3/3, split, running output pointer
             case 4: return 34;   // 12x3/2, split, running output pointer, hoisted xy sums (+8 % over 15)
             case 5: return 27;   // 8x4, level 0 re-read from the ring (slots 4), split
-            case 6: return 40;   // level split over two CTAs, 12x3/2 hoisted each (3 levels per CTA)
-            case 8: return 40;   // level split over two CTAs, 12x3/2 hoisted each (4 levels per CTA)
+            case 6: return 48;   // level split over two CTAs, 12x3 hoisted, role-swapped 2-slot queue each
+            case 8: return 48;   // the same (4 levels per CTA); +3-5 % over 40
             default: return 12;  // 8x4/2, split
         }
     }
@@ -210,7 +210,12 @@ bool is_usable(int v) {
         case 41: return usable<R, T, 41>();
         case 42: return usable<R, T, 42>();
         case 43: return usable<R, T, 43>();
-        default: return usable<R, T, 44>();
+        case 44: return usable<R, T, 44>();
+        case 45: return usable<R, T, 45>();
+        case 46: return usable<R, T, 46>();
+        case 47: return usable<R, T, 47>();
+        case 48: return usable<R, T, 48>();
+        default: return usable<R, T, 49>();
     }
 }
 

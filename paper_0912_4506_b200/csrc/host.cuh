@@ -105,8 +105,14 @@ constexpr Variant kVariants[] = {
     {10, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 1},   // 42
     {11, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 1},   // 43
     {10, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 0},   // 44
+    // role-swapped 2-slot queues (slots 5): one move per value instead of two
+    {12, 3, 5, 1, 8, 1, 1, 0, 1, 1, 1, 3},   // 45: 34 role-swapped
+    {8, 4, 5, 2, 8, 0, 1, 80},               // 46: 9 role-swapped
+    {8, 8, 5, 1, 8, 1, 0, 128},              // 47: fp32: 8 role-swapped
+    {12, 3, 5, 1, 8, 1, 1, 0, 1, 2, 1, 3},   // 48: 40 role-swapped
+    {12, 6, 5, 1, 8, 1, 0, 128, 1, 1, 1, 3}, // 49: fp32: 37 role-swapped
 };
-constexpr int kNumVariants = 45;
+constexpr int kNumVariants = 50;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -132,6 +138,11 @@ constexpr bool compiled() {
     if (V >= 36 && V <= 38) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V >= 39 && V <= 41) return T == 4 || T == 6 || T == 8;
     if (V >= 42 && V <= 44) return sizeof(R) == 8 && T >= 3 && T <= 5;
+    if (V == 45) return T >= 3 && T <= 4;
+    if (V == 46) return T == 2;
+    if (V == 47) return sizeof(R) == 4 && T >= 2 && T <= 4;
+    if (V == 48) return T == 4 || T == 6 || T == 8;
+    if (V == 49) return sizeof(R) == 4 && T >= 3 && T <= 4;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -284,7 +295,12 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 41: return launch_tb_t<R, T, 41>(src, L, a, grid, s);
         case 42: return launch_tb_t<R, T, 42>(src, L, a, grid, s);
         case 43: return launch_tb_t<R, T, 43>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 44>(src, L, a, grid, s);
+        case 44: return launch_tb_t<R, T, 44>(src, L, a, grid, s);
+        case 45: return launch_tb_t<R, T, 45>(src, L, a, grid, s);
+        case 46: return launch_tb_t<R, T, 46>(src, L, a, grid, s);
+        case 47: return launch_tb_t<R, T, 47>(src, L, a, grid, s);
+        case 48: return launch_tb_t<R, T, 48>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 49>(src, L, a, grid, s);
     }
 }
 

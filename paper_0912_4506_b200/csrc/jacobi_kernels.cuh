@@ -410,8 +410,13 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     // step parity (the set loaded in step k is v[p-1] in step k+1), so level
     // 0 needs no queue moves.
     constexpr bool L0C = SLOTS == 4;
-    constexpr int QS = L0C ? 2 : SLOTS;
-    static_assert(SLOTS >= 1 && SLOTS <= 4, "z-queue slots");
+    // SLOTS = 5: the 2-slot queue with the slot ROLES swapping every step
+    // (steps unrolled by 2): v[p] stays where it is and becomes next step's
+    // v[p-1]; only the new plane moves into the dead v[p-1] slot -- one
+    // register move per value instead of two.
+    constexpr bool RSW = SLOTS == 5;
+    constexpr int QS = (L0C || RSW) ? 2 : SLOTS;
+    static_assert(SLOTS >= 1 && SLOTS <= 5, "z-queue slots");
     static_assert(!INPL || (CL == 1 && LS == 1 && !PEER), "in-place passes: single-CTA variants");
     static_assert(LS == 1 || (T % LS == 0 && CL == 1 && !PEER && QS != 1),
                   "level split: depth a multiple of the cluster size");
@@ -632,8 +637,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         // queues by reference, i.e. through local memory
         auto step = [&](auto phase, auto fast, int st) __attribute__((always_inline)) {
             constexpr int PH = decltype(phase)::value;
-            constexpr int F0 = QS == 3 ? PH : 0;                               // v[p-1]
-            constexpr int F1 = QS == 3 ? (PH + 1) % 3 : (QS == 1 ? PH : 1);    // v[p]
+            constexpr int F0 = QS == 3 ? PH : (RSW ? PH : 0);                                 // v[p-1]
+            constexpr int F1 = QS == 3 ? (PH + 1) % 3 : (QS == 1 ? PH : (RSW ? PH ^ 1 : 1));  // v[p]
             constexpr int F2 = QS == 3 ? (PH + 2) % 3 : (QS == 1 ? PH ^ 1 : 0); // v[p+1]
             // L0C: this step's level-0 v[p] lands in M0[PH ^ 1]; M0[PH] is v[p-1]
             constexpr int C0 = L0C ? (PH ^ 1) : 0, M0I = L0C ? PH : 0;
@@ -783,7 +788,9 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                         const R upd = ups[i];
                         if constexpr (FAST) dst[j][i] = upd;
                         else dst[j][i] = ((inm >> (j * PX + i)) & 1u) ? upd : cc[j][i];
-                        if constexpr (QS == 2) {   // shift level t-1's queue
+                        if constexpr (RSW) {       // the new plane into the consumed v[p-1] slot
+                            Q[F0][t - 1][j][i] = nn[j][i];
+                        } else if constexpr (QS == 2) {   // shift level t-1's queue
                             if (!L0C || t > 1) {
                                 Q[0][t - 1][j][i] = cc[j][i];
                                 Q[1][t - 1][j][i] = nn[j][i];
@@ -906,7 +913,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         // Steps [fs, fe) are FAST for the whole warp (zin_all is an interval in
         // st); they run as a branch-free loop unrolled by the z-queue period, the
         // rest step by step with a per-step FAST/SLOW choice.
-        constexpr int PER = (QS == 1 || L0C) ? 2 : (QS == 3 ? 3 : 1);
+        constexpr int PER = (QS == 1 || L0C || RSW) ? 2 : (QS == 3 ? 3 : 1);
         using I0 = std::integral_constant<int, 0>;
         using I1 = std::integral_constant<int, PER >= 2 ? 1 : 0>;
         using I2 = std::integral_constant<int, PER >= 3 ? 2 : 0>;
