@@ -145,7 +145,8 @@ int default_variant(int dtype, int T) {
             case 1: return 5;    // 16x2/3, ring 6
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
             case 3: return 21;   // 12x3/3, split, running output pointer
-            case 4: return 34;   // 12x3/2, split, running output pointer, hoisted xy sums (+8 % over 15)
+            case 4: return 15;   // 8x4/3, split, running output pointer (after the branch-free FAST loop:
+                                 // 776-787 vs 749-757 for 34, 12x3/2 hoisted)
             case 5: return 27;   // 8x4, level 0 re-read from the ring (slots 4), split
             case 6: return 48;   // level split over two CTAs, 12x3 hoisted, role-swapped 2-slot queue each
             case 8: return 48;   // the same (4 levels per CTA); +3-5 % over 40
@@ -157,8 +158,9 @@ int default_variant(int dtype, int T) {
         case 2: return 16;       // 8x8/2, two CTAs per SM, split
         case 3: return 37;       // 12x6/2, running output pointer, hoisted xy sums (+3.5 % over 22)
         case 4: return 8;        // 8x8/2, running output pointer
-        case 5:
-        case 6: return 11;       // 16x2/2, split
+        case 5: return 11;       // 16x2/2, split
+        case 6: return 51;       // level split over two CTAs, 16x4/2 hoisted each (64x64): 1158 vs 889
+        case 8: return 52;       // level split over two CTAs, 8x8 role-swapped (64x64): 1279 vs 860
         default: return 2;       // 8x4/2
     }
 }
@@ -215,7 +217,10 @@ bool is_usable(int v) {
         case 46: return usable<R, T, 46>();
         case 47: return usable<R, T, 47>();
         case 48: return usable<R, T, 48>();
-        default: return usable<R, T, 49>();
+        case 49: return usable<R, T, 49>();
+        case 50: return usable<R, T, 50>();
+        case 51: return usable<R, T, 51>();
+        default: return usable<R, T, 52>();
     }
 }
 

@@ -111,8 +111,12 @@ constexpr Variant kVariants[] = {
     {8, 8, 5, 1, 8, 1, 0, 128},              // 47: fp32: 8 role-swapped
     {12, 3, 5, 1, 8, 1, 1, 0, 1, 2, 1, 3},   // 48: 40 role-swapped
     {12, 6, 5, 1, 8, 1, 0, 128, 1, 1, 1, 3}, // 49: fp32: 37 role-swapped
+    // level split with 64x64 footprints (T=4: two levels per CTA, 1.33 cell-levels per useful one)
+    {8, 8, 2, 1, 8, 1, 1, 0, 1, 2, 1, 3},    // 50: 8 warps x 8 rows per CTA
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 2, 1, 3},   // 51: 16 warps x 4 rows per CTA
+    {8, 8, 5, 1, 8, 1, 1, 0, 1, 2, 1, 3},    // 52: 50 role-swapped
 };
-constexpr int kNumVariants = 50;
+constexpr int kNumVariants = 53;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -143,6 +147,7 @@ constexpr bool compiled() {
     if (V == 47) return sizeof(R) == 4 && T >= 2 && T <= 4;
     if (V == 48) return T == 4 || T == 6 || T == 8;
     if (V == 49) return sizeof(R) == 4 && T >= 3 && T <= 4;
+    if (V >= 50 && V <= 52) return T == 4 || T == 6 || T == 8;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -300,7 +305,10 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 46: return launch_tb_t<R, T, 46>(src, L, a, grid, s);
         case 47: return launch_tb_t<R, T, 47>(src, L, a, grid, s);
         case 48: return launch_tb_t<R, T, 48>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 49>(src, L, a, grid, s);
+        case 49: return launch_tb_t<R, T, 49>(src, L, a, grid, s);
+        case 50: return launch_tb_t<R, T, 50>(src, L, a, grid, s);
+        case 51: return launch_tb_t<R, T, 51>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 52>(src, L, a, grid, s);
     }
 }
 
