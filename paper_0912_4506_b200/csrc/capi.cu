@@ -98,6 +98,30 @@ int check_layout(const sp_layout* L, int dtype) {
     return SP_OK;
 }
 
+// Y-strip scratch (saved rows between the tiles of a strip, YS variants): one
+// growing device buffer per (device, stream) -- launches on a stream are
+// serial, launches on different streams never share one.  Never freed.
+int strip_scratch(cudaStream_t stream, size_t bytes, void** out) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, uintptr_t, std::thread::id>, std::pair<void*, size_t>> bufs;
+    int dev = 0;
+    SP_CUDA(cudaGetDevice(&dev));
+    const std::thread::id tid = stream == cudaStreamPerThread ? std::this_thread::get_id() : std::thread::id();
+    const auto key = std::make_tuple(dev, reinterpret_cast<uintptr_t>(stream), tid);
+    std::lock_guard<std::mutex> lock(mu);
+    auto& e = bufs[key];
+    if (e.second < bytes) {
+        if (e.first) SP_CUDA(cudaStreamSynchronize(stream));   // an earlier pass may still read it
+        if (e.first) SP_CUDA(cudaFree(e.first));
+        e.first = nullptr;
+        e.second = 0;
+        SP_CUDA(cudaMalloc(&e.first, bytes));
+        e.second = bytes;
+    }
+    *out = e.first;
+    return SP_OK;
+}
+
 // Dynamic-schedule unit counters: one per (device, stream).  Launches on one
 // stream run one after another and every K2 launch leaves its counter at zero
 // again (the last CTA to overshoot re-arms it), so a stream's launches can
@@ -220,7 +244,15 @@ bool is_usable(int v) {
         case 49: return usable<R, T, 49>();
         case 50: return usable<R, T, 50>();
         case 51: return usable<R, T, 51>();
-        default: return usable<R, T, 52>();
+        case 52: return usable<R, T, 52>();
+        case 53: return usable<R, T, 53>();
+        case 54: return usable<R, T, 54>();
+        case 55: return usable<R, T, 55>();
+        case 56: return usable<R, T, 56>();
+        case 57: return usable<R, T, 57>();
+        case 58: return usable<R, T, 58>();
+        case 59: return usable<R, T, 59>();
+        default: return usable<R, T, 60>();
     }
 }
 
@@ -586,7 +618,7 @@ int sp_describe_variant(int dtype, int T, char* buf, int buflen) {
                  k.rstore ? ", running output pointer" : "",
                  k.ls > 1 ? (k.ls == 2 ? ", level split over a 2-CTA cluster" : ", level split over a 4-CTA cluster")
                           : "",
-                 k.cl > 1 ? ", y-cooperative cluster" : "");
+                 k.cl > 1 ? ", y-cooperative cluster" : k.ys > 0 ? ", y strips (saved rows, no bottom halo)" : "");
     }
     return v;
 }
@@ -785,9 +817,21 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     const int cl = kVariants[variant].cl;
     const int wy = kVariants[variant].by * kVariants[variant].py * cl;   // cluster footprint rows
     if (wy - 2 * T < 1) return fail(SP_ERR_SCHEDULE, "depth T=%d too deep for a %d-row footprint", T, wy);
+    const int ys = kVariants[variant].ys;
+    a.ys_len = 0;
+    a.sv_steps = 0;
+    a.ysave = nullptr;
     a.oy = wy - 2 * T;
+    if (ys > 0) {
+        // y strips: a tile's outputs start at its first footprint row (the row below
+        // comes from the previous tile), so only the top halo remains; a strip of ys
+        // tiles outputs ys*oy rows minus the T-1 its first tile computes from nothing
+        a.oy = wy - T;
+        a.ys_len = ys * a.oy - (T - 1);
+        if (a.ys_len < 1) return fail(SP_ERR_SCHEDULE, "y strip of %d tiles too short for T=%d", ys, T);
+    }
     a.ntx = (int)((out_hi[2] - out_lo[2] + a.ox - 1) / a.ox);
-    a.nty = (int)((out_hi[1] - out_lo[1] + a.oy - 1) / a.oy);
+    a.nty = (int)((out_hi[1] - out_lo[1] + (ys > 0 ? a.ys_len : a.oy) - 1) / (ys > 0 ? a.ys_len : a.oy));
     a.gy = (int)L->gy;
     a.gz = (int)L->gz;
     const int64_t nzb = out_hi[0] - out_lo[0];
@@ -847,6 +891,12 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
     }
     int grid = (int)std::min<int64_t>(a.units, slots);
     cudaStream_t s = (cudaStream_t)stream;
+    if (ys > 0) {
+        a.sv_steps = (int)(len + 2 * T);
+        const size_t bytes = (size_t)grid * a.sv_steps * (T - 1) * sp::WX * elem_size(dtype);
+        rc = strip_scratch(s, bytes, &a.ysave);
+        if (rc) return rc;
+    }
     a.rd_lo = a.rd_hi = 0;
     a.rz_lo = INT32_MIN;
     a.rz_hi = INT32_MAX;

@@ -48,6 +48,7 @@ struct Variant {
     int ls = 1;                      // 2: level-split pipeline over a cluster of two CTAs
     int lag = 1;                     // 2: lag-2 z-wavefront (tb2_kernel, wave2.cuh)
     int hoist = 0;                   // xy-sum placement in the step (see tb_kernel HOIST)
+    int ys = 0;                      // > 0: y strips of this many tiles (saved rows, no bottom halo)
 };
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
@@ -115,8 +116,18 @@ constexpr Variant kVariants[] = {
     {8, 8, 2, 1, 8, 1, 1, 0, 1, 2, 1, 3},    // 50: 8 warps x 8 rows per CTA
     {16, 4, 2, 1, 8, 1, 1, 0, 1, 2, 1, 3},   // 51: 16 warps x 4 rows per CTA
     {8, 8, 5, 1, 8, 1, 1, 0, 1, 2, 1, 3},    // 52: 50 role-swapped
+    {8, 4, 3, 1, 8, 1, 1, 0, 1, 1, 1, 1},    // 53: 15 with level 1's sums before the TMA wait
+    {8, 4, 5, 1, 8, 1, 1},                   // 54: 15's shape, role-swapped 2-slot queue
+    {8, 4, 3, 1, 6, 1, 1},                   // 55: 15 with a 6-plane ring
+    // y strips: tiles of a strip run bottom to top, the row below each footprint
+    // comes from the previous tile (no bottom halo): fewer redundant cell-levels
+    {8, 4, 3, 1, 8, 1, 1, 0, 1, 1, 1, 0, 4},   // 56: 15 in strips of 4 tiles
+    {12, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 4},  // 57: 34 in strips of 4
+    {8, 4, 3, 1, 8, 1, 1, 0, 1, 1, 1, 0, 8},   // 58: 15 in strips of 8
+    {12, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 0, 4},  // 59: 21 in strips of 4
+    {8, 8, 2, 1, 8, 1, 0, 128, 1, 1, 1, 0, 4}, // 60: fp32: 8 in strips of 4
 };
-constexpr int kNumVariants = 53;
+constexpr int kNumVariants = 61;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -148,6 +159,9 @@ constexpr bool compiled() {
     if (V == 48) return T == 4 || T == 6 || T == 8;
     if (V == 49) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V >= 50 && V <= 52) return T == 4 || T == 6 || T == 8;
+    if (V >= 53 && V <= 55) return sizeof(R) == 8 && T >= 3 && T <= 4;
+    if (V >= 56 && V <= 59) return sizeof(R) == 8 && T >= 2 && T <= 4;
+    if (V == 60) return sizeof(R) == 4 && T >= 2 && T <= 4;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -167,7 +181,7 @@ constexpr bool usable() {
         return T >= 2 && sp::Plan2<R, T, v.by, v.py, v.minb, v.ring>::FITS;
     } else {
         // level split: each CTA holds T/ls levels; the footprint still carries the T halo
-        return sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>::FITS &&
+        return sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls, v.ys>::FITS &&
                v.by * v.py * v.cl - 2 * T >= 1;
     }
 }
@@ -181,12 +195,12 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         constexpr Variant v = kVariants[V];
         static_assert(v.lag == 1 || (!PEER && !INPL), "lag-2 variants: two-grid passes only");
         using Pl = std::conditional_t<v.lag == 2, sp::Plan2<R, T, v.by, v.py, v.minb, v.ring>,
-                                      sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls>>;
+                                      sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls, v.ys>>;
         auto kern = [] {
             constexpr Variant w = kVariants[V];
             if constexpr (w.lag == 2) return sp::tb2_kernel<R, T, w.by, w.py, w.minb, w.ring>;
             else return sp::tb_kernel<R, T, w.by, w.py, w.slots, w.minb, w.ring, w.rstore, w.split, PEER, w.cl,
-                                      w.ls, INPL, w.hoist>;
+                                      w.ls, INPL, w.hoist, w.ys>;
         }();
         const size_t smem = Pl::SMEM;
         // the >48 KB dynamic shared-memory opt-in is a per-device function attribute
@@ -211,6 +225,18 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                          SP_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+        CUtensorMap map_sv = map;   // y strips: the saved rows [CTA * steps][T-1][WX]
+        if constexpr (v.ys > 0 && v.lag == 1) {
+            constexpr int NLV = T / v.ls - 1;
+            if (!a.ysave || a.sv_steps < 1) return fail(SP_ERR_ARG, "y-strip pass without its scratch");
+            cuuint64_t sdim[3] = {(cuuint64_t)sp::WX, (cuuint64_t)NLV, (cuuint64_t)grid * (cuuint64_t)a.sv_steps};
+            cuuint64_t sstr[2] = {(cuuint64_t)(sp::WX * sizeof(R)), (cuuint64_t)(NLV * sp::WX * sizeof(R))};
+            cuuint32_t sbox[3] = {(cuuint32_t)sp::WX, (cuuint32_t)NLV, 1};
+            r = enc(&map_sv, sizeof(R) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                    a.ysave, sdim, sstr, sbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled (saved rows) failed (%d)", (int)r);
+        }
         if constexpr (v.cl > 1 || v.ls > 1) {
             constexpr int csize = v.cl > 1 ? v.cl : v.ls;
             // persistent clusters: as many as can be co-resident, round-robin units
@@ -241,9 +267,11 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
             }
             const int clusters = (int)std::min<int64_t>(a.units, (int64_t)(nc - 1));
             cfg.gridDim = dim3(clusters * csize, 1, 1);
-            SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a));
+            if constexpr (v.lag == 2) SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a));
+            else SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, map_sv, a));
         } else {
-            kern<<<grid, Pl::NT, smem, stream>>>(map, a);
+            if constexpr (v.lag == 2) kern<<<grid, Pl::NT, smem, stream>>>(map, a);
+            else kern<<<grid, Pl::NT, smem, stream>>>(map, map_sv, a);
         }
         g_launches.fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
@@ -308,7 +336,15 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 49: return launch_tb_t<R, T, 49>(src, L, a, grid, s);
         case 50: return launch_tb_t<R, T, 50>(src, L, a, grid, s);
         case 51: return launch_tb_t<R, T, 51>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 52>(src, L, a, grid, s);
+        case 52: return launch_tb_t<R, T, 52>(src, L, a, grid, s);
+        case 53: return launch_tb_t<R, T, 53>(src, L, a, grid, s);
+        case 54: return launch_tb_t<R, T, 54>(src, L, a, grid, s);
+        case 55: return launch_tb_t<R, T, 55>(src, L, a, grid, s);
+        case 56: return launch_tb_t<R, T, 56>(src, L, a, grid, s);
+        case 57: return launch_tb_t<R, T, 57>(src, L, a, grid, s);
+        case 58: return launch_tb_t<R, T, 58>(src, L, a, grid, s);
+        case 59: return launch_tb_t<R, T, 59>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 60>(src, L, a, grid, s);
     }
 }
 

@@ -68,6 +68,12 @@ struct TBArgs {
     // planes it overwrites (c-2, c-3; c+2, c+3 in reverse) are complete.
     int zshift, reverse, nch;
     unsigned* cdone;           // null: not in place
+    // y strips (YS > 0): a unit is a strip of up to YS tiles processed bottom to top;
+    // each tile saves, per step, the row the next tile needs below its footprint
+    // (levels 1..T-1) in `ysave` [CTA][step][level][WX], read back by TMA.
+    int ys_len;                // output rows of a strip (0: no strips)
+    int sv_steps;              // steps per tile in the ysave layout (>= chunk + 2T)
+    void* ysave;
 };
 
 // ---- small PTX helpers ------------------------------------------------------
@@ -329,7 +335,7 @@ __device__ __forceinline__ Unit decode_unit(const TBArgs& a, int u) {
     Unit w;
     w.c = c;
     w.x0 = a.olo[2] + tx * a.ox;
-    w.y0 = a.olo[1] + ty * a.oy;
+    w.y0 = a.olo[1] + ty * (a.ys_len ? a.ys_len : a.oy);
     w.zc0 = a.olo[0] + c * a.chunk_len;
     w.zc1 = min(w.zc0 + a.chunk_len, a.ohi[0]);
     return w;
@@ -348,7 +354,7 @@ __device__ __forceinline__ int footprint_x(const TBArgs& a, int x0, int T) {
 // planes plus, for levels 1..T-1, one plane each -- double-buffered when it
 // fits (one barrier per step), single-buffered otherwise (two barriers).
 template <typename R, int T, int BY, int PY, int SLOTS = 3, int MINB = 1, int RCAP = 8, int CL = 1,
-          int LS = 1>
+          int LS = 1, int YS = 0>
 struct Plan {
     // SLOTS == 1 keeps only v[p] in registers; v[p-1] is re-read from the
     // double-buffered level plane (and ring slot k-2) just before it is
@@ -361,7 +367,10 @@ struct Plan {
     // Clusters (CL > 1): the ring's level-0 planes carry HR extra rows above
     // and below the CTA's rows (level 1's y-neighbours at the CTA edges);
     // deeper levels take them from the neighbour CTAs' level planes (DSMEM).
-    static constexpr int HR = CL > 1 ? 1 : 0;
+    static constexpr int HR = (CL > 1 || YS > 0) ? 1 : 0;
+    // YS > 0: per ring slot, the saved rows of levels 1..T-1 (TMA from ysave)
+    static constexpr int SVPLANE = YS > 0 ? (T - 1) * WX : 0;
+    static constexpr int SV_BYTES = SVPLANE * (int)sizeof(R);
     static constexpr int RROWS = WY + 2 * HR;
     static constexpr int RPLANE = WX * RROWS;
     static constexpr int RPLANE_BYTES = RPLANE * (int)sizeof(R);
@@ -370,16 +379,17 @@ struct Plan {
     static constexpr int NL = (T > 1) ? (T - 1) : 0;        // stored level planes
     static constexpr bool DB = 2 * NL * PLANE_BYTES + 3 * RPLANE_BYTES <= BUDGET;
     static constexpr int NBUF = DB ? 2 : 1;
-    static constexpr int RING_FIT = (BUDGET - NBUF * NL * PLANE_BYTES) / RPLANE_BYTES;
+    static constexpr int RING_FIT = (BUDGET - NBUF * NL * PLANE_BYTES) / (RPLANE_BYTES + SV_BYTES);
     static constexpr int RING = RING_FIT > RCAP ? RCAP : RING_FIT;
     static constexpr int MIN_RING = SLOTS == 1 ? 4 : 3;
     static constexpr bool FITS = RING >= MIN_RING && CL * WY - 2 * T >= 1 && (SLOTS != 1 || DB) &&
-                                 (CL == 1 || (DB && SLOTS != 1 && T >= 2));
+                                 (CL == 1 || (DB && SLOTS != 1 && T >= 2)) &&
+                                 (YS == 0 || (DB && T >= 2 && CL == 1 && LS == 1));
     static constexpr int NUID = 16;   // unit ids handed from the producer to the consumers
     // LS > 1: T here is the depth one CTA holds; RING more mbarriers ("slot
     // consumed" of the next CTA's ring)
     static constexpr int NEMPTY = LS > 1 ? RING : 0;
-    static constexpr size_t SMEM = (size_t)RING * RPLANE_BYTES + (size_t)NBUF * NL * PLANE_BYTES +
+    static constexpr size_t SMEM = (size_t)RING * (RPLANE_BYTES + SV_BYTES) + (size_t)NBUF * NL * PLANE_BYTES +
                                    (RING + 2 + NEMPTY) * 8 + NUID * 4;
 };
 
@@ -402,9 +412,10 @@ struct Plan {
 // CTA keeps only D levels of z-queue in registers, so T=8 fits where one CTA
 // holding all eight levels spills.
 template <typename R, int T, int BY, int PY, int SLOTS, int MINB, int RCAP, int RSTORE, int SPLITV,
-          bool PEER = false, int CL = 1, int LS = 1, bool INPL = false, int HOIST = 0>
+          bool PEER = false, int CL = 1, int LS = 1, bool INPL = false, int HOIST = 0, int YS = 0>
 __global__ void __launch_bounds__(32 * BY, MINB)
-    tb_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
+    tb_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_sv,
+              const TBArgs a) {
     // SLOTS = 4: levels >= 1 as SLOTS = 2; level 0's v[p] is re-read from the
     // ring every step into one of two register sets that alternate with the
     // step parity (the set loaded in step k is v[p-1] in step k+1), so level
@@ -424,11 +435,15 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     constexpr int QN = QS == 1 ? 2 : QS;         // register slots per level
     using A = Arith<R>;
     using V2 = typename A::V2;
-    using P = Plan<R, D, BY, PY, SLOTS, MINB, RCAP, CL, LS>;
+    static_assert(YS == 0 || (!INPL && !PEER && CL == 1 && LS == 1), "y strips: plain two-grid passes");
+    using P = Plan<R, D, BY, PY, SLOTS, MINB, RCAP, CL, LS, YS>;
     constexpr int WY = P::WY;
     constexpr int PLANE = P::PLANE;
     constexpr int RPLANE = P::RPLANE;
     constexpr int HR = P::HR;
+    // YS: the warp and patch row holding footprint row oy-1 = WY-T-1 (saved for the next tile)
+    constexpr int YS_W = YS > 0 ? (WY - T - 1) / PY : 0;
+    constexpr int YS_J = YS > 0 ? (WY - T - 1) % PY : 0;
     constexpr int RING_N = P::RING;
     static_assert(CL == 1 || (SPLITV && P::DB && QS != 1 && T >= 2 && !PEER),
                   "cluster variants need the split barrier, double-buffered planes, 2-3 slots");
@@ -436,7 +451,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     R* ring = reinterpret_cast<R*>(smem_raw);
     R* lvl = ring + RING_N * RPLANE;  // [level-1][buf] planes for levels 1..T-1
-    uint64_t* full = reinterpret_cast<uint64_t*>(lvl + P::NBUF * P::NL * PLANE);
+    R* sv = lvl + P::NBUF * P::NL * PLANE;   // [RING][T-1][WX] saved rows (YS)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sv + RING_N * P::SVPLANE);
     uint64_t* lbar = full + RING_N;   // [2]: step-parity barriers of the level planes (SPLIT)
     uint64_t* empty = lbar + 2;       // [NEMPTY] (LS > 1, rank 0): rank 1 consumed ring slot i
     volatile int* uid = reinterpret_cast<volatile int*>(empty + P::NEMPTY);
@@ -500,7 +516,14 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     // plain arrive completes the next slot's phase so the consumers can read
     // the end marker (-1).
     int pu = -1, pseq = 0, pc0 = 0, pc1 = 0, pc2 = 0, pc2_end = 0;
+    int pk = 0, pnt = 1, pst = 0, pc2_beg = 0;   // YS: tile in the strip, tiles, step in the tile
     bool pdone = false;
+    // YS: the footprint rows of tile k of the strip starting at output row y0 (the
+    // first tile starts T-1 rows early: its lowest outputs read unwritten saved rows)
+    auto strip_tiles = [&](const Unit& w) -> int {
+        const int top = min(w.y0 + a.ys_len, a.ohi[1]);
+        return min(YS > 0 ? YS : 1, (top - (w.y0 - (T - 1)) + a.oy - 1) / a.oy);
+    };
     auto producer_unit = [&]() {
         if constexpr (CL > 1 || LS > 1) {
             pu = pseq == 0 ? (int)cluster_id_x() : pu + (int)cluster_count_x();
@@ -515,9 +538,10 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         if (pu >= a.units) return;
         const Unit pw = decode_unit<INPL>(a, pu);
         pc0 = footprint_x<R>(a, pw.x0, T) + a.x_off;
-        pc1 = pw.y0 - T + crank * WY - HR + a.gy;
-        pc2 = pw.zc0 - Te + a.gz;
+        pc1 = (YS > 0 ? pw.y0 - (T - 1) : pw.y0 - T + crank * WY) - HR + a.gy;
+        pc2 = pc2_beg = pw.zc0 - Te + a.gz;
         pc2_end = pw.zc1 + Te + a.gz;
+        if constexpr (YS > 0) { pk = 0; pst = 0; pnt = strip_tiles(pw); }
     };
     if (threadIdx.x == 0) producer_unit();
     auto produce = [&](int slot) {
@@ -526,13 +550,29 @@ __global__ void __launch_bounds__(32 * BY, MINB)
             pdone = true;
             return;
         }
-        mbar_expect_tx(&full[slot], kRingBytes);
+        mbar_expect_tx(&full[slot], kRingBytes + (uint32_t)P::SV_BYTES);
         if (LS == 1 || first) tma_load_3d(ring + slot * RPLANE, &tmap, &full[slot], pc0, pc1, pc2);
         else mbar_arrive_remote_cta(pv_empty + 8u * slot);   // rank r-1 may fill this slot (see above)
-        if (++pc2 == pc2_end) producer_unit();
+        if constexpr (YS > 0) {
+            // the rows the previous tile saved one step earlier (step 0: unused, any row)
+            tma_load_3d(sv + slot * P::SVPLANE, &tmap_sv, &full[slot], 0, 0,
+                        (int)blockIdx.x * a.sv_steps + max(pst - 1, 0));
+            ++pst;
+        }
+        if (++pc2 == pc2_end) {
+            if (YS > 0 && ++pk < pnt) {   // next tile of the strip: same z range, oy rows up
+                pc2 = pc2_beg;
+                pc1 += a.oy;
+                pst = 0;
+            } else {
+                producer_unit();
+            }
+        }
     };
     if (threadIdx.x == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+        if constexpr (YS > 0)
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_sv)) : "memory");
         // the slot released after step k is k-1 (k-2 with SLOTS == 1): prime the rest
         for (int i = 0; i < RING_N - (QS == 1 ? 2 : 1); ++i) produce(i);
     }
@@ -550,396 +590,430 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         const int u = uid[cseq & (P::NUID - 1)];
         if (u < 0) break;
         const Unit w = decode_unit<INPL>(a, u);
-        const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T + crank * WY;
-        const int nsteps = (w.zc1 - w.zc0) + 2 * Te;
+        // y strips: the unit's tiles bottom to top (one tile otherwise)
+        const int ntile = YS > 0 ? strip_tiles(w) : 1;
+        for (int kt = 0; kt < ntile; ++kt) {
+            const int fx = footprint_x<R>(a, w.x0, T);
+            const int fy = YS > 0 ? w.y0 - (T - 1) + kt * a.oy : w.y0 - T + crank * WY;
+            // output rows of this tile: the first tile of a strip starts T-1 rows low
+            // (rows it computed from unwritten saved rows), strips end at ys_len
+            const int oylo = YS > 0 ? max(fy, w.y0) : w.y0;
+            const int oyhi = YS > 0 ? min(min(fy + a.oy, w.y0 + a.ys_len), a.ohi[1]) : min(w.y0 + a.oy, a.ohi[1]);
+            const int nsteps = (w.zc1 - w.zc0) + 2 * Te;
 
-        // Per-level x/y domain of this thread's columns: x bits (PX per level)
-        // and y bits (PY per level); `fastm` bit t-1 = every cell of this
-        // WARP lies in level t's x/y domain (then the Dirichlet select is
-        // skipped warp-uniformly).
-        uint32_t xin = 0;
-        uint64_t yin = 0;   // D*PY bits (up to 64)
-        uint32_t fastm = 0;
-#pragma unroll
-        for (int t = 1; t <= D; ++t) {
-            const int ext = T - L0 - t;   // level L0+t's domain extension
-            int xl = a.lo[2] - a.elo[2] * ext, xh = a.hi[2] + a.ehi[2] * ext;
-            int yl = a.lo[1] - a.elo[1] * ext, yh = a.hi[1] + a.ehi[1] * ext;
-            bool all = true;
-#pragma unroll
+            // Per-level x/y domain of this thread's columns: x bits (PX per level)
+            // and y bits (PY per level); `fastm` bit t-1 = every cell of this
+            // WARP lies in level t's x/y domain (then the Dirichlet select is
+            // skipped warp-uniformly).
+            uint32_t xin = 0;
+            uint64_t yin = 0;   // D*PY bits (up to 64)
+            uint32_t fastm = 0;
+    #pragma unroll
+            for (int t = 1; t <= D; ++t) {
+                const int ext = T - L0 - t;   // level L0+t's domain extension
+                int xl = a.lo[2] - a.elo[2] * ext, xh = a.hi[2] + a.ehi[2] * ext;
+                int yl = a.lo[1] - a.elo[1] * ext, yh = a.hi[1] + a.ehi[1] * ext;
+                bool all = true;
+    #pragma unroll
+                for (int i = 0; i < PX; ++i) {
+                    int gx = fx + cx + i;
+                    bool in = gx >= xl && gx < xh;
+                    all &= in;
+                    if (in) xin |= 1u << ((t - 1) * PX + i);
+                }
+    #pragma unroll
+                for (int j = 0; j < PY; ++j) {
+                    int gyy = fy + cy + j;
+                    bool in = gyy >= yl && gyy < yh;
+                    all &= in;
+                    if (in) yin |= 1ull << ((t - 1) * PY + j);
+                }
+                if (__all_sync(0xffffffffu, all)) fastm |= 1u << (t - 1);
+            }
+            // level-T write masks: inside this tile's output region and the box.
+            uint32_t wx = 0, wyb = 0;
+    #pragma unroll
             for (int i = 0; i < PX; ++i) {
                 int gx = fx + cx + i;
-                bool in = gx >= xl && gx < xh;
-                all &= in;
-                if (in) xin |= 1u << ((t - 1) * PX + i);
+                wx |= (gx >= w.x0 && gx < min(w.x0 + a.ox, a.ohi[2]) ? 1u : 0u) << i;
             }
-#pragma unroll
+    #pragma unroll
             for (int j = 0; j < PY; ++j) {
                 int gyy = fy + cy + j;
-                bool in = gyy >= yl && gyy < yh;
-                all &= in;
-                if (in) yin |= 1ull << ((t - 1) * PY + j);
+                wyb |= (gyy >= oylo && gyy < oyhi ? 1u : 0u) << j;
             }
-            if (__all_sync(0xffffffffu, all)) fastm |= 1u << (t - 1);
-        }
-        // level-T write masks: inside this tile's output region and the box.
-        uint32_t wx = 0, wyb = 0;
-#pragma unroll
-        for (int i = 0; i < PX; ++i) {
-            int gx = fx + cx + i;
-            wx |= (gx >= w.x0 && gx < min(w.x0 + a.ox, a.ohi[2]) ? 1u : 0u) << i;
-        }
-#pragma unroll
-        for (int j = 0; j < PY; ++j) {
-            int gyy = fy + cy + j;
-            wyb |= (gyy >= w.y0 && gyy < min(w.y0 + a.oy, a.ohi[1]) ? 1u : 0u) << j;
-        }
-        R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
-        const int64_t pz = a.pz, py = a.py;
-        // INPL: level-T plane p goes to plane p + zshift (compressed storage)
-        const int zsh = INPL ? a.zshift : 0;
-        R* dnext = dcol + (int64_t)(w.zc0 - Te - D + zsh) * pz;   // plane q-D of step 0
-        // both x cells written and the pair 16-byte aligned (same for every row: py is)
-        const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
-        // every row of the patch is written with one 16-byte store (interior tiles)
-        const bool full_rows = vec_store && wyb == (1u << PY) - 1u;
+            R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
+            const int64_t pz = a.pz, py = a.py;
+            // INPL: level-T plane p goes to plane p + zshift (compressed storage)
+            const int zsh = INPL ? a.zshift : 0;
+            R* dnext = dcol + (int64_t)(w.zc0 - Te - D + zsh) * pz;   // plane q-D of step 0
+            // both x cells written and the pair 16-byte aligned (same for every row: py is)
+            const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
+            // every row of the patch is written with one 16-byte store (interior tiles)
+            const bool full_rows = vec_store && wyb == (1u << PY) - 1u;
 
-        // Per level t < T, a register z-queue.  SLOTS == 3: three slots
-        // rotating with the step phase -- at phase f, Q[f] = v[p-1],
-        // Q[f+1] = v[p], and the new plane v[p+1] lands in Q[f+2]; steps are
-        // unrolled by 3, so there are no register moves.  SLOTS == 2: Q[0] =
-        // v[p-1], Q[1] = v[p], the new plane lives in a transient and the
-        // queue shifts by moves (fewer live registers, more instructions).
-        // SLOTS == 1: Q[f] = v[p] and Q[f^1] = v[p+1] (new), steps unrolled by 2;
-        // v[p-1] comes back from shared memory.
-        R Q[QN][D][PY][PX];
-        R M0[L0C ? 2 : 1][PY][PX];   // L0C: level 0's v[p-1] / v[p] by step parity
-#pragma unroll
-        for (int f = 0; f < (L0C ? 2 : 1); ++f)
-#pragma unroll
-            for (int j = 0; j < PY; ++j)
-#pragma unroll
-                for (int i = 0; i < PX; ++i) M0[f][j][i] = R(0);
-#pragma unroll
-        for (int f = 0; f < QN; ++f)
-#pragma unroll
-            for (int t = 0; t < D; ++t)
-#pragma unroll
+            // Per level t < T, a register z-queue.  SLOTS == 3: three slots
+            // rotating with the step phase -- at phase f, Q[f] = v[p-1],
+            // Q[f+1] = v[p], and the new plane v[p+1] lands in Q[f+2]; steps are
+            // unrolled by 3, so there are no register moves.  SLOTS == 2: Q[0] =
+            // v[p-1], Q[1] = v[p], the new plane lives in a transient and the
+            // queue shifts by moves (fewer live registers, more instructions).
+            // SLOTS == 1: Q[f] = v[p] and Q[f^1] = v[p+1] (new), steps unrolled by 2;
+            // v[p-1] comes back from shared memory.
+            R Q[QN][D][PY][PX];
+            R M0[L0C ? 2 : 1][PY][PX];   // L0C: level 0's v[p-1] / v[p] by step parity
+    #pragma unroll
+            for (int f = 0; f < (L0C ? 2 : 1); ++f)
+    #pragma unroll
                 for (int j = 0; j < PY; ++j)
-#pragma unroll
-                    for (int i = 0; i < PX; ++i) Q[f][t][j][i] = R(0);
-
-        // One z-step.  FAST (warp-uniform, decided per step): every cell of
-        // the warp is inside every level's domain this step, so the update is
-        // straight-line; otherwise cells outside D_t keep their previous-level
-        // value (Dirichlet walls, rank faces) through a per-cell select.
-        // always inlined: a step that became a call would take the register
-        // queues by reference, i.e. through local memory
-        auto step = [&](auto phase, auto fast, int st) __attribute__((always_inline)) {
-            constexpr int PH = decltype(phase)::value;
-            constexpr int F0 = QS == 3 ? PH : (RSW ? PH : 0);                                 // v[p-1]
-            constexpr int F1 = QS == 3 ? (PH + 1) % 3 : (QS == 1 ? PH : (RSW ? PH ^ 1 : 1));  // v[p]
-            constexpr int F2 = QS == 3 ? (PH + 2) % 3 : (QS == 1 ? PH ^ 1 : 0); // v[p+1]
-            // L0C: this step's level-0 v[p] lands in M0[PH ^ 1]; M0[PH] is v[p-1]
-            constexpr int C0 = L0C ? (PH ^ 1) : 0, M0I = L0C ? PH : 0;
-            constexpr bool FAST = decltype(fast)::value;
-
-            const int slot = gstep % RING_N;
-            const int pslot = (gstep + RING_N - 1) % RING_N;
-            const int pslot2 = (gstep + RING_N - 2) % RING_N;
-            const int cur = P::DB ? (int)(gstep & 1u) : 0;
-            const int prv = P::DB ? cur ^ 1 : 0;
-            const int q = w.zc0 - Te + st;
-            if constexpr (L0C) {   // level 0 at plane q-1 (ring slot of the previous step)
-                const R* Lc = ring + pslot * RPLANE + HR * WX;
-#pragma unroll
-                for (int j = 0; j < PY; ++j) {
-                    V2 r = *reinterpret_cast<const V2*>(Lc + (cy + j) * WX + cx);
-                    M0[C0][j][0] = r.x;
-                    M0[C0][j][1] = r.y;
-                }
-            }
-            auto qcur = [&](int t) __attribute__((always_inline)) -> const R(&)[PY][PX] {   // level t's v[p]
-                if constexpr (L0C) return t == 0 ? M0[C0] : Q[F1][t];
-                else return Q[F1][t];
-            };
-
-            // s_t = (x- + x+) + (y- + y+) of level t-1 at plane q-t, produced in
-            // the previous step (ring slot pslot / level buffer prv; own and
-            // lane-neighbour cells from the registers of Q[F1]).
-            R s[D][PY][PX];
-            auto xy_sums = [&](int t) __attribute__((always_inline)) {
-                const R* Pl = (t == 1) ? ring + pslot * RPLANE + HR * WX
-                                       : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
-                const R(&v)[PY][PX] = qcur(t - 1);
-                V2 up, dn;
-                if constexpr (CL > 1) {
-                    // level 0: the ring's halo rows; deeper: the neighbour slice's
-                    // edge row of the previous step (DSMEM), own slice otherwise
-                    const uint32_t off = (uint32_t)((((t - 2) * P::NBUF + prv) * PLANE + cx) * sizeof(R));
-                    if (t == 1) up = SmemLd<R>::v2(Pl + (cy - 1) * WX + cx);
-                    else if (wy == 0 && has_up) up = DsmemLd<R>::v2(up_lvl + off + (WY - 1) * WX * sizeof(R));
-                    else up = SmemLd<R>::v2(Pl + cym * WX + cx);
-                    if (t == 1) dn = SmemLd<R>::v2(Pl + (cy + PY) * WX + cx);
-                    else if (wy == BY - 1 && has_dn) dn = DsmemLd<R>::v2(dn_lvl + off);
-                    else dn = SmemLd<R>::v2(Pl + cyp * WX + cx);
-                } else {
-                    up = *reinterpret_cast<const V2*>(Pl + cym * WX + cx);
-                    dn = *reinterpret_cast<const V2*>(Pl + cyp * WX + cx);
-                }
-#pragma unroll
-                for (int j = 0; j < PY; ++j) {
-                    R lft = __shfl_up_sync(0xffffffffu, v[j][1], 1);
-                    R rgt = __shfl_down_sync(0xffffffffu, v[j][0], 1);
-                    R ym0 = (j == 0) ? up.x : v[j > 0 ? j - 1 : 0][0];
-                    R ym1 = (j == 0) ? up.y : v[j > 0 ? j - 1 : 0][1];
-                    R yp0 = (j == PY - 1) ? dn.x : v[j + 1 < PY ? j + 1 : j][0];
-                    R yp1 = (j == PY - 1) ? dn.y : v[j + 1 < PY ? j + 1 : j][1];
-                    // ((x- + x+) + (y- + y+)): the x sums pair a lane neighbour's
-                    // cell with our own (scalar adds write them as a pair), the
-                    // y sums and the total are pair ops
-                    if constexpr (!PACK) {
-                        s[t - 1][j][0] = A::add(A::add(lft, v[j][1]), A::add(ym0, yp0));
-                        s[t - 1][j][1] = A::add(A::add(v[j][0], rgt), A::add(ym1, yp1));
-                    } else {
-                        R x0 = A::add(lft, v[j][1]), x1 = A::add(v[j][0], rgt), y0, y1;
-                        A::add2(y0, y1, ym0, ym1, yp0, yp1);
-                        A::add2(s[t - 1][j][0], s[t - 1][j][1], x0, x1, y0, y1);
-                    }
-                }
-            };
-            if constexpr (!P::DB) {
-#pragma unroll
-                for (int t = 1; t <= D; ++t) xy_sums(t);
-                __syncthreads();   // single buffers: all reads before any overwrite
-            }
-
-            // HOIST bit 0: level 1's xy sums (level 0 of the previous plane, already
-            // in the ring) before waiting for this step's TMA plane
-            if constexpr (P::DB && (HOIST & 1)) xy_sums(1);
-            mbar_wait(&full[slot], (gstep / RING_N) & 1);
-            // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
-            R Nt[QS == 2 ? D : 1][PY][PX];
-            auto newv = [&](int t) __attribute__((always_inline)) -> R(&)[PY][PX] {
-                if constexpr (QS != 2) return Q[F2][t];
-                else return Nt[t];
-            };
-            // QS == 1: v[p-1] of level t-1, re-read from shared memory
-            R mv[QS == 1 ? PY : 1][PX];
-            if constexpr (QS == 1) {
-                const R* L2 = ring + pslot2 * RPLANE;   // level 0, plane q-2
-#pragma unroll
-                for (int j = 0; j < PY; ++j) {
-                    V2 r = *reinterpret_cast<const V2*>(L2 + (cy + j) * WX + cx);
-                    mv[j][0] = r.x;
-                    mv[j][1] = r.y;
-                }
-            }
-            {
-                const R* L0 = ring + slot * RPLANE + HR * WX;
-                R(&n0)[PY][PX] = newv(0);
-#pragma unroll
-                for (int j = 0; j < PY; ++j) {
-                    V2 r = *reinterpret_cast<const V2*>(L0 + (cy + j) * WX + cx);
-                    n0[j][0] = r.x;
-                    n0[j][1] = r.y;
-                }
-            }
-            R out[PY][PX];  // level-D values of plane q-D
-#pragma unroll
-            for (int t = 1; t <= D; ++t) {
-                if constexpr (P::DB) {
-                    if (t == 1 ? !(HOIST & 1) : !(HOIST & 2)) xy_sums(t);
-                }
-                const R(&mm)[PY][PX] = *([&]() -> const R(*)[PY][PX] {
-                    if constexpr (QS == 1) return &mv;
-                    else if constexpr (L0C) return t == 1 ? &M0[M0I] : &Q[F0][t - 1];
-                    else return &Q[F0][t - 1];
-                }());
-                const R(&cc)[PY][PX] = qcur(t - 1);
-                const R(&nn)[PY][PX] = newv(t - 1);
-                R(&dst)[PY][PX] = (t < D) ? newv(t < D ? t : 0) : out;
-                uint32_t inm = 0;   // SLOW: one bit per cell, in D_t this step
-                if constexpr (!FAST) {
-                    const int p = q - t;
-                    const int ext = T - L0 - t;
-                    const bool zin = p >= a.lo[0] - a.elo[0] * ext && p < a.hi[0] + a.ehi[0] * ext;
-                    const uint32_t xb = (xin >> ((t - 1) * PX)) & ((1u << PX) - 1);
-                    const uint32_t yb = (uint32_t)(yin >> ((t - 1) * PY)) & ((1u << PY) - 1);
-#pragma unroll
+    #pragma unroll
+                    for (int i = 0; i < PX; ++i) M0[f][j][i] = R(0);
+    #pragma unroll
+            for (int f = 0; f < QN; ++f)
+    #pragma unroll
+                for (int t = 0; t < D; ++t)
+    #pragma unroll
                     for (int j = 0; j < PY; ++j)
-                        if (zin && ((yb >> j) & 1u)) inm |= xb << (j * PX);
-                }
-#pragma unroll
-                for (int j = 0; j < PY; ++j) {
-                    // (s + (z- + z+)) * ONE_SIXTH for the pair (PX == 2)
-                    R zs[PX], us[PX], ups[PX];
-                    if constexpr (!PACK) {
-#pragma unroll
-                        for (int i = 0; i < PX; ++i)
-                            ups[i] = A::mul(A::add(s[t - 1][j][i], A::add(mm[j][i], nn[j][i])), sixth);
-                    } else {
-                        A::add2(zs[0], zs[1], mm[j][0], mm[j][1], nn[j][0], nn[j][1]);
-                        A::add2(us[0], us[1], s[t - 1][j][0], s[t - 1][j][1], zs[0], zs[1]);
-                        A::mul2(ups[0], ups[1], us[0], us[1], sixth);
+    #pragma unroll
+                        for (int i = 0; i < PX; ++i) Q[f][t][j][i] = R(0);
+
+            // One z-step.  FAST (warp-uniform, decided per step): every cell of
+            // the warp is inside every level's domain this step, so the update is
+            // straight-line; otherwise cells outside D_t keep their previous-level
+            // value (Dirichlet walls, rank faces) through a per-cell select.
+            // always inlined: a step that became a call would take the register
+            // queues by reference, i.e. through local memory
+            auto step = [&](auto phase, auto fast, int st) __attribute__((always_inline)) {
+                constexpr int PH = decltype(phase)::value;
+                constexpr int F0 = QS == 3 ? PH : (RSW ? PH : 0);                                 // v[p-1]
+                constexpr int F1 = QS == 3 ? (PH + 1) % 3 : (QS == 1 ? PH : (RSW ? PH ^ 1 : 1));  // v[p]
+                constexpr int F2 = QS == 3 ? (PH + 2) % 3 : (QS == 1 ? PH ^ 1 : 0); // v[p+1]
+                // L0C: this step's level-0 v[p] lands in M0[PH ^ 1]; M0[PH] is v[p-1]
+                constexpr int C0 = L0C ? (PH ^ 1) : 0, M0I = L0C ? PH : 0;
+                constexpr bool FAST = decltype(fast)::value;
+
+                const int slot = gstep % RING_N;
+                const int pslot = (gstep + RING_N - 1) % RING_N;
+                const int pslot2 = (gstep + RING_N - 2) % RING_N;
+                const int cur = P::DB ? (int)(gstep & 1u) : 0;
+                const int prv = P::DB ? cur ^ 1 : 0;
+                const int q = w.zc0 - Te + st;
+                if constexpr (L0C) {   // level 0 at plane q-1 (ring slot of the previous step)
+                    const R* Lc = ring + pslot * RPLANE + HR * WX;
+    #pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        V2 r = *reinterpret_cast<const V2*>(Lc + (cy + j) * WX + cx);
+                        M0[C0][j][0] = r.x;
+                        M0[C0][j][1] = r.y;
                     }
-#pragma unroll
-                    for (int i = 0; i < PX; ++i) {
-                        const R upd = ups[i];
-                        if constexpr (FAST) dst[j][i] = upd;
-                        else dst[j][i] = ((inm >> (j * PX + i)) & 1u) ? upd : cc[j][i];
-                        if constexpr (RSW) {       // the new plane into the consumed v[p-1] slot
-                            Q[F0][t - 1][j][i] = nn[j][i];
-                        } else if constexpr (QS == 2) {   // shift level t-1's queue
-                            if (!L0C || t > 1) {
-                                Q[0][t - 1][j][i] = cc[j][i];
-                                Q[1][t - 1][j][i] = nn[j][i];
-                            }
+                }
+                auto qcur = [&](int t) __attribute__((always_inline)) -> const R(&)[PY][PX] {   // level t's v[p]
+                    if constexpr (L0C) return t == 0 ? M0[C0] : Q[F1][t];
+                    else return Q[F1][t];
+                };
+
+                // s_t = (x- + x+) + (y- + y+) of level t-1 at plane q-t, produced in
+                // the previous step (ring slot pslot / level buffer prv; own and
+                // lane-neighbour cells from the registers of Q[F1]).
+                R s[D][PY][PX];
+                auto xy_sums = [&](int t) __attribute__((always_inline)) {
+                    const R* Pl = (t == 1) ? ring + pslot * RPLANE + HR * WX
+                                           : lvl + ((t - 2) * P::NBUF + prv) * PLANE;
+                    const R(&v)[PY][PX] = qcur(t - 1);
+                    V2 up, dn;
+                    if constexpr (CL > 1) {
+                        // level 0: the ring's halo rows; deeper: the neighbour slice's
+                        // edge row of the previous step (DSMEM), own slice otherwise
+                        const uint32_t off = (uint32_t)((((t - 2) * P::NBUF + prv) * PLANE + cx) * sizeof(R));
+                        if (t == 1) up = SmemLd<R>::v2(Pl + (cy - 1) * WX + cx);
+                        else if (wy == 0 && has_up) up = DsmemLd<R>::v2(up_lvl + off + (WY - 1) * WX * sizeof(R));
+                        else up = SmemLd<R>::v2(Pl + cym * WX + cx);
+                        if (t == 1) dn = SmemLd<R>::v2(Pl + (cy + PY) * WX + cx);
+                        else if (wy == BY - 1 && has_dn) dn = DsmemLd<R>::v2(dn_lvl + off);
+                        else dn = SmemLd<R>::v2(Pl + cyp * WX + cx);
+                    } else if constexpr (YS > 0) {
+                        // level 0: the ring's rows -1 and WY; deeper: warp 0's row below
+                        // the footprint is the previous tile's saved row (TMA'd into sv
+                        // with this step's plane), the top warp's clamps (top halo)
+                        if (t == 1) {
+                            up = *reinterpret_cast<const V2*>(Pl + (cy - 1) * WX + cx);
+                            dn = *reinterpret_cast<const V2*>(Pl + (cy + PY) * WX + cx);
+                        } else {
+                            up = wy == 0 ? *reinterpret_cast<const V2*>(sv + slot * P::SVPLANE + (t - 2) * WX + cx)
+                                         : *reinterpret_cast<const V2*>(Pl + cym * WX + cx);
+                            dn = *reinterpret_cast<const V2*>(Pl + cyp * WX + cx);
                         }
-                    }
-                }
-                if (SPLIT && t == 1 && gstep > 0) {
-                    // step k-1 is complete in every warp: its reads of this
-                    // buffer are done and its level planes are visible
-                    const uint32_t k1 = gstep - 1;
-                    // only the edge warps read a neighbour's planes: cluster-scope acquire
-                    if (CL > 1 && ((wy == 0 && has_up) || (wy == BY - 1 && has_dn)))
-                        mbar_wait_cluster(&lbar[k1 & 1u], (k1 >> 1) & 1u);
-                    else
-                        mbar_wait(&lbar[k1 & 1u], (k1 >> 1) & 1u);
-                    if (threadIdx.x == 0) {
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        // ring slot last read in step k-1: plane k-2 (k-3 with SLOTS == 1,
-                        // which re-reads v[p-1] from slot k-2 at the start of a step)
-                        produce(QS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
-                    }
-                }
-                // HOIST bit 1: every deeper level's xy sums at once, right after step
-                // k-1's level planes are known complete (independent DADD chains)
-                if constexpr (P::DB && (HOIST & 2)) {
-                    if (t == 1) {
-#pragma unroll
-                        for (int tt = 2; tt <= D; ++tt) xy_sums(tt);
-                    }
-                }
-                if (t < D) {
-                    R* Pl = lvl + ((t - 1) * P::NBUF + cur) * PLANE;
-                    if constexpr (QS == 1) {
-                        // this buffer still holds level t at plane q-t-1 = v[p-1]
-                        // of level t+1: read it back, then store the full new plane
-#pragma unroll
-                        for (int j = 0; j < PY; ++j) {
-                            V2 r = *reinterpret_cast<const V2*>(Pl + (cy + j) * WX + cx);
-                            mv[j][0] = r.x;
-                            mv[j][1] = r.y;
-                        }
-#pragma unroll
-                        for (int j = 0; j < PY; ++j)
-                            *reinterpret_cast<V2*>(Pl + (cy + j) * WX + cx) = V2{dst[j][0], dst[j][1]};
                     } else {
-                        *reinterpret_cast<V2*>(Pl + cy * WX + cx) = V2{dst[0][0], dst[0][1]};
-                        if (PY > 1)
-                            *reinterpret_cast<V2*>(Pl + (cy + PY - 1) * WX + cx) =
-                                V2{dst[PY - 1][0], dst[PY - 1][1]};
+                        up = *reinterpret_cast<const V2*>(Pl + cym * WX + cx);
+                        dn = *reinterpret_cast<const V2*>(Pl + cyp * WX + cx);
                     }
-                }
-            }
-            // level T: write the finished plane (once the pipeline is full).
-            // RSTORE: dnext points at plane q-T of this thread's patch and
-            // advances one plane per step; otherwise the address is formed per
-            // step.  Both are bit-identical -- ptxas schedules them differently
-            // and the tuned variant table picks per (dtype, T).
-            if (LS > 1 && !last && st >= 2 * D) {
-                // level L0+D of plane q-D -> the next rank's ring, once it has freed the slot
-                const uint32_t s1 = gsent % RING_N;
-                mbar_wait(&empty[s1], (gsent / RING_N) & 1);
-                const uint32_t base = nx_ring + (uint32_t)((s1 * RPLANE + cy * WX + cx) * sizeof(R));
-#pragma unroll
-                for (int j = 0; j < PY; ++j)
-                    StAsync<R>::v2(base + (uint32_t)(j * WX * sizeof(R)), out[j][0], out[j][1], nx_full + 8u * s1);
-                ++gsent;
-            } else if (st >= 2 * D) {
-                R* d = RSTORE ? dnext : dcol + (int64_t)(q - D + zsh) * pz;
-                auto put = [&](R* b) {
-                    if (full_rows) {
-#pragma unroll
-                        for (int j = 0; j < PY; ++j)
-                            __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
-                    } else if (vec_store) {
-#pragma unroll
-                        for (int j = 0; j < PY; ++j)
-                            if ((wyb >> j) & 1u)
-                                __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
-                    } else if (wx != 0u) {   // lanes with no output column skip the whole block
-#pragma unroll
-                        for (int j = 0; j < PY; ++j) {
-                            const bool row = (wyb >> j) & 1u;
-                            if (row && (wx & 1u)) __stcs(b + j * py, out[j][0]);
-                            if (row && (wx & 2u)) __stcs(b + j * py + 1, out[j][1]);
+    #pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        R lft = __shfl_up_sync(0xffffffffu, v[j][1], 1);
+                        R rgt = __shfl_down_sync(0xffffffffu, v[j][0], 1);
+                        R ym0 = (j == 0) ? up.x : v[j > 0 ? j - 1 : 0][0];
+                        R ym1 = (j == 0) ? up.y : v[j > 0 ? j - 1 : 0][1];
+                        R yp0 = (j == PY - 1) ? dn.x : v[j + 1 < PY ? j + 1 : j][0];
+                        R yp1 = (j == PY - 1) ? dn.y : v[j + 1 < PY ? j + 1 : j][1];
+                        // ((x- + x+) + (y- + y+)): the x sums pair a lane neighbour's
+                        // cell with our own (scalar adds write them as a pair), the
+                        // y sums and the total are pair ops
+                        if constexpr (!PACK) {
+                            s[t - 1][j][0] = A::add(A::add(lft, v[j][1]), A::add(ym0, yp0));
+                            s[t - 1][j][1] = A::add(A::add(v[j][0], rgt), A::add(ym1, yp1));
+                        } else {
+                            R x0 = A::add(lft, v[j][1]), x1 = A::add(v[j][0], rgt), y0, y1;
+                            A::add2(y0, y1, ym0, ym1, yp0, yp1);
+                            A::add2(s[t - 1][j][0], s[t - 1][j][1], x0, x1, y0, y1);
                         }
                     }
                 };
-                put(d);
-                if constexpr (PEER) {   // the same plane into a neighbour's ghost plane
-                    const int p = q - D;
-                    if (p < a.rz_lo) put(d + a.rd_lo);
-                    if (p >= a.rz_hi) put(d + a.rd_hi);
+                if constexpr (!P::DB) {
+    #pragma unroll
+                    for (int t = 1; t <= D; ++t) xy_sums(t);
+                    __syncthreads();   // single buffers: all reads before any overwrite
                 }
-            }
-            if (RSTORE) dnext += pz;
-            if constexpr (SPLIT) {
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&lbar[gstep & 1u]);
-                    if constexpr (CL > 1) {
-                        // our edge rows of this step are stored / the neighbour's are read
-                        if (wy == 0 && has_up) mbar_arrive_remote(up_lbar + 8u * (gstep & 1u));
-                        if (wy == BY - 1 && has_dn) mbar_arrive_remote(dn_lbar + 8u * (gstep & 1u));
+
+                // HOIST bit 0: level 1's xy sums (level 0 of the previous plane, already
+                // in the ring) before waiting for this step's TMA plane
+                if constexpr (P::DB && (HOIST & 1)) xy_sums(1);
+                mbar_wait(&full[slot], (gstep / RING_N) & 1);
+                // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
+                R Nt[QS == 2 ? D : 1][PY][PX];
+                auto newv = [&](int t) __attribute__((always_inline)) -> R(&)[PY][PX] {
+                    if constexpr (QS != 2) return Q[F2][t];
+                    else return Nt[t];
+                };
+                // QS == 1: v[p-1] of level t-1, re-read from shared memory
+                R mv[QS == 1 ? PY : 1][PX];
+                if constexpr (QS == 1) {
+                    const R* L2 = ring + pslot2 * RPLANE;   // level 0, plane q-2
+    #pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        V2 r = *reinterpret_cast<const V2*>(L2 + (cy + j) * WX + cx);
+                        mv[j][0] = r.x;
+                        mv[j][1] = r.y;
                     }
                 }
-            } else {
-                __syncthreads();
-                // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
-                if (threadIdx.x == 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    produce(QS == 1 ? pslot2 : pslot);
+                {
+                    const R* L0 = ring + slot * RPLANE + HR * WX;
+                    R(&n0)[PY][PX] = newv(0);
+    #pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        V2 r = *reinterpret_cast<const V2*>(L0 + (cy + j) * WX + cx);
+                        n0[j][0] = r.x;
+                        n0[j][1] = r.y;
+                    }
                 }
+                R out[PY][PX];  // level-D values of plane q-D
+    #pragma unroll
+                for (int t = 1; t <= D; ++t) {
+                    if constexpr (P::DB) {
+                        if (t == 1 ? !(HOIST & 1) : !(HOIST & 2)) xy_sums(t);
+                    }
+                    const R(&mm)[PY][PX] = *([&]() -> const R(*)[PY][PX] {
+                        if constexpr (QS == 1) return &mv;
+                        else if constexpr (L0C) return t == 1 ? &M0[M0I] : &Q[F0][t - 1];
+                        else return &Q[F0][t - 1];
+                    }());
+                    const R(&cc)[PY][PX] = qcur(t - 1);
+                    const R(&nn)[PY][PX] = newv(t - 1);
+                    R(&dst)[PY][PX] = (t < D) ? newv(t < D ? t : 0) : out;
+                    uint32_t inm = 0;   // SLOW: one bit per cell, in D_t this step
+                    if constexpr (!FAST) {
+                        const int p = q - t;
+                        const int ext = T - L0 - t;
+                        const bool zin = p >= a.lo[0] - a.elo[0] * ext && p < a.hi[0] + a.ehi[0] * ext;
+                        const uint32_t xb = (xin >> ((t - 1) * PX)) & ((1u << PX) - 1);
+                        const uint32_t yb = (uint32_t)(yin >> ((t - 1) * PY)) & ((1u << PY) - 1);
+    #pragma unroll
+                        for (int j = 0; j < PY; ++j)
+                            if (zin && ((yb >> j) & 1u)) inm |= xb << (j * PX);
+                    }
+    #pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        // (s + (z- + z+)) * ONE_SIXTH for the pair (PX == 2)
+                        R zs[PX], us[PX], ups[PX];
+                        if constexpr (!PACK) {
+    #pragma unroll
+                            for (int i = 0; i < PX; ++i)
+                                ups[i] = A::mul(A::add(s[t - 1][j][i], A::add(mm[j][i], nn[j][i])), sixth);
+                        } else {
+                            A::add2(zs[0], zs[1], mm[j][0], mm[j][1], nn[j][0], nn[j][1]);
+                            A::add2(us[0], us[1], s[t - 1][j][0], s[t - 1][j][1], zs[0], zs[1]);
+                            A::mul2(ups[0], ups[1], us[0], us[1], sixth);
+                        }
+    #pragma unroll
+                        for (int i = 0; i < PX; ++i) {
+                            const R upd = ups[i];
+                            if constexpr (FAST) dst[j][i] = upd;
+                            else dst[j][i] = ((inm >> (j * PX + i)) & 1u) ? upd : cc[j][i];
+                            if constexpr (RSW) {       // the new plane into the consumed v[p-1] slot
+                                Q[F0][t - 1][j][i] = nn[j][i];
+                            } else if constexpr (QS == 2) {   // shift level t-1's queue
+                                if (!L0C || t > 1) {
+                                    Q[0][t - 1][j][i] = cc[j][i];
+                                    Q[1][t - 1][j][i] = nn[j][i];
+                                }
+                            }
+                        }
+                    }
+                    if (SPLIT && t == 1 && gstep > 0) {
+                        // step k-1 is complete in every warp: its reads of this
+                        // buffer are done and its level planes are visible
+                        const uint32_t k1 = gstep - 1;
+                        // only the edge warps read a neighbour's planes: cluster-scope acquire
+                        if (CL > 1 && ((wy == 0 && has_up) || (wy == BY - 1 && has_dn)))
+                            mbar_wait_cluster(&lbar[k1 & 1u], (k1 >> 1) & 1u);
+                        else
+                            mbar_wait(&lbar[k1 & 1u], (k1 >> 1) & 1u);
+                        if (threadIdx.x == 0) {
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                            // ring slot last read in step k-1: plane k-2 (k-3 with SLOTS == 1,
+                            // which re-reads v[p-1] from slot k-2 at the start of a step)
+                            produce(QS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
+                        }
+                    }
+                    // HOIST bit 1: every deeper level's xy sums at once, right after step
+                    // k-1's level planes are known complete (independent DADD chains)
+                    if constexpr (P::DB && (HOIST & 2)) {
+                        if (t == 1) {
+    #pragma unroll
+                            for (int tt = 2; tt <= D; ++tt) xy_sums(tt);
+                        }
+                    }
+                    if constexpr (YS > 0) {
+                        // the row the next tile of the strip reads below its footprint
+                        if (t < D && wy == YS_W) {
+                            R* g = reinterpret_cast<R*>(a.ysave) +
+                                   ((int64_t)blockIdx.x * a.sv_steps + st) * (D - 1) * WX + (t - 1) * WX + cx;
+                            *reinterpret_cast<V2*>(g) = V2{dst[YS_J][0], dst[YS_J][1]};
+                        }
+                    }
+                    if (t < D) {
+                        R* Pl = lvl + ((t - 1) * P::NBUF + cur) * PLANE;
+                        if constexpr (QS == 1) {
+                            // this buffer still holds level t at plane q-t-1 = v[p-1]
+                            // of level t+1: read it back, then store the full new plane
+    #pragma unroll
+                            for (int j = 0; j < PY; ++j) {
+                                V2 r = *reinterpret_cast<const V2*>(Pl + (cy + j) * WX + cx);
+                                mv[j][0] = r.x;
+                                mv[j][1] = r.y;
+                            }
+    #pragma unroll
+                            for (int j = 0; j < PY; ++j)
+                                *reinterpret_cast<V2*>(Pl + (cy + j) * WX + cx) = V2{dst[j][0], dst[j][1]};
+                        } else {
+                            *reinterpret_cast<V2*>(Pl + cy * WX + cx) = V2{dst[0][0], dst[0][1]};
+                            if (PY > 1)
+                                *reinterpret_cast<V2*>(Pl + (cy + PY - 1) * WX + cx) =
+                                    V2{dst[PY - 1][0], dst[PY - 1][1]};
+                        }
+                    }
+                }
+                // level T: write the finished plane (once the pipeline is full).
+                // RSTORE: dnext points at plane q-T of this thread's patch and
+                // advances one plane per step; otherwise the address is formed per
+                // step.  Both are bit-identical -- ptxas schedules them differently
+                // and the tuned variant table picks per (dtype, T).
+                if (LS > 1 && !last && st >= 2 * D) {
+                    // level L0+D of plane q-D -> the next rank's ring, once it has freed the slot
+                    const uint32_t s1 = gsent % RING_N;
+                    mbar_wait(&empty[s1], (gsent / RING_N) & 1);
+                    const uint32_t base = nx_ring + (uint32_t)((s1 * RPLANE + cy * WX + cx) * sizeof(R));
+    #pragma unroll
+                    for (int j = 0; j < PY; ++j)
+                        StAsync<R>::v2(base + (uint32_t)(j * WX * sizeof(R)), out[j][0], out[j][1], nx_full + 8u * s1);
+                    ++gsent;
+                } else if (st >= 2 * D) {
+                    R* d = RSTORE ? dnext : dcol + (int64_t)(q - D + zsh) * pz;
+                    auto put = [&](R* b) {
+                        if (full_rows) {
+    #pragma unroll
+                            for (int j = 0; j < PY; ++j)
+                                __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
+                        } else if (vec_store) {
+    #pragma unroll
+                            for (int j = 0; j < PY; ++j)
+                                if ((wyb >> j) & 1u)
+                                    __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
+                        } else if (wx != 0u) {   // lanes with no output column skip the whole block
+    #pragma unroll
+                            for (int j = 0; j < PY; ++j) {
+                                const bool row = (wyb >> j) & 1u;
+                                if (row && (wx & 1u)) __stcs(b + j * py, out[j][0]);
+                                if (row && (wx & 2u)) __stcs(b + j * py + 1, out[j][1]);
+                            }
+                        }
+                    };
+                    put(d);
+                    if constexpr (PEER) {   // the same plane into a neighbour's ghost plane
+                        const int p = q - D;
+                        if (p < a.rz_lo) put(d + a.rd_lo);
+                        if (p >= a.rz_hi) put(d + a.rd_hi);
+                    }
+                }
+                if (RSTORE) dnext += pz;
+#ifndef SP_NO_SVFENCE
+                if constexpr (YS > 0) {   // saved rows -> visible to the TMA (async proxy) reads
+                    if (wy == YS_W) asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+#endif
+                if constexpr (SPLIT) {
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive(&lbar[gstep & 1u]);
+                        if constexpr (CL > 1) {
+                            // our edge rows of this step are stored / the neighbour's are read
+                            if (wy == 0 && has_up) mbar_arrive_remote(up_lbar + 8u * (gstep & 1u));
+                            if (wy == BY - 1 && has_dn) mbar_arrive_remote(dn_lbar + 8u * (gstep & 1u));
+                        }
+                    }
+                } else {
+                    __syncthreads();
+                    // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
+                    if (threadIdx.x == 0) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        produce(QS == 1 ? pslot2 : pslot);
+                    }
+                }
+                ++gstep;
+            };
+            // warp-uniform: the whole warp is inside every level's x/y domain
+            const bool fast_xy = fastm == (1u << D) - 1u;
+            // planes q-t of every level inside its z domain <=> st in [fs, fe) below
+            // Steps [fs, fe) are FAST for the whole warp (zin_all is an interval in
+            // st); they run as a branch-free loop unrolled by the z-queue period, the
+            // rest step by step with a per-step FAST/SLOW choice.
+            constexpr int PER = (QS == 1 || L0C || RSW) ? 2 : (QS == 3 ? 3 : 1);
+            using I0 = std::integral_constant<int, 0>;
+            using I1 = std::integral_constant<int, PER >= 2 ? 1 : 0>;
+            using I2 = std::integral_constant<int, PER >= 3 ? 2 : 0>;
+            auto one = [&](auto fast, int st) __attribute__((always_inline)) {
+                const int ph = PER == 1 ? 0 : st % PER;
+                if (ph == 0) step(I0{}, fast, st);
+                else if (PER >= 2 && ph == 1) step(I1{}, fast, st);
+                else if (PER >= 3) step(I2{}, fast, st);
+            };
+            int fs = nsteps, fe = nsteps;
+            if (fast_xy) {
+                const int q0 = w.zc0 - Te;    // q of step 0
+                fs = max(0, a.lo[0] + D - q0);
+                fe = min(nsteps, a.hi[0] + a.ehi[0] * (T - L0 - 1) + 1 - q0);
+                if (fe <= fs) fs = fe = nsteps;
             }
-            ++gstep;
-        };
-        // warp-uniform: the whole warp is inside every level's x/y domain
-        const bool fast_xy = fastm == (1u << D) - 1u;
-        // planes q-t of every level inside its z domain <=> st in [fs, fe) below
-        // Steps [fs, fe) are FAST for the whole warp (zin_all is an interval in
-        // st); they run as a branch-free loop unrolled by the z-queue period, the
-        // rest step by step with a per-step FAST/SLOW choice.
-        constexpr int PER = (QS == 1 || L0C || RSW) ? 2 : (QS == 3 ? 3 : 1);
-        using I0 = std::integral_constant<int, 0>;
-        using I1 = std::integral_constant<int, PER >= 2 ? 1 : 0>;
-        using I2 = std::integral_constant<int, PER >= 3 ? 2 : 0>;
-        auto one = [&](auto fast, int st) __attribute__((always_inline)) {
-            const int ph = PER == 1 ? 0 : st % PER;
-            if (ph == 0) step(I0{}, fast, st);
-            else if (PER >= 2 && ph == 1) step(I1{}, fast, st);
-            else if (PER >= 3) step(I2{}, fast, st);
-        };
-        int fs = nsteps, fe = nsteps;
-        if (fast_xy) {
-            const int q0 = w.zc0 - Te;    // q of step 0
-            fs = max(0, a.lo[0] + D - q0);
-            fe = min(nsteps, a.hi[0] + a.ehi[0] * (T - L0 - 1) + 1 - q0);
-            if (fe <= fs) fs = fe = nsteps;
-        }
-        int st = 0;
-        for (; st < fs; ++st) one(std::false_type{}, st);
-        for (; st < fe && st % PER != 0; ++st) one(std::true_type{}, st);
-        for (; st + PER <= fe; st += PER) {
-            step(I0{}, std::true_type{}, st);
-            if constexpr (PER >= 2) step(I1{}, std::true_type{}, st + 1);
-            if constexpr (PER >= 3) step(I2{}, std::true_type{}, st + 2);
-        }
-        for (; st < fe; ++st) one(std::true_type{}, st);
-        for (; st < nsteps; ++st) one(std::false_type{}, st);
+            int st = 0;
+            for (; st < fs; ++st) one(std::false_type{}, st);
+            for (; st < fe && st % PER != 0; ++st) one(std::true_type{}, st);
+            for (; st + PER <= fe; st += PER) {
+                step(I0{}, std::true_type{}, st);
+                if constexpr (PER >= 2) step(I1{}, std::true_type{}, st + 1);
+                if constexpr (PER >= 3) step(I2{}, std::true_type{}, st + 2);
+            }
+            for (; st < fe; ++st) one(std::true_type{}, st);
+            for (; st < nsteps; ++st) one(std::false_type{}, st);
+        }   // tiles of the strip
         if constexpr (INPL) {
             if (threadIdx.x == 0) {
                 // this thread consumed the unit's last plane: all its global reads (TMA) are done
