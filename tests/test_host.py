@@ -187,7 +187,9 @@ def test_describe_variant_defaults(sp):
     assert "12 warps x 3 rows" in d[(N.SP_F64, 3)]
     assert "level split over a 2-CTA cluster" in d[(N.SP_F64, 8)]
     assert "level split" in d[(N.SP_F64, 6)]
-    assert "level split" not in d[(N.SP_F32, 8)]
+    assert "level split" in d[(N.SP_F32, 8)] and "64x64 footprint" in d[(N.SP_F32, 8)]
+    assert "8 warps x 4 rows" in d[(N.SP_F64, 4)] and "3-slot" in d[(N.SP_F64, 4)]
+    assert "level split" not in d[(N.SP_F32, 4)]
     with pytest.raises(ValueError):
         N.describe_variant(N.SP_F64, 9)
 
