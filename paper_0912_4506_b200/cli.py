@@ -209,6 +209,10 @@ def cmd_bench(args) -> int:
             except ReferenceUnavailable:
                 verified = "skipped"
         results.append(BenchResult("gpu-" + variant, dims, cfg, args.sweeps, seconds, updates, verified))
+        if args.dump:                                   # R/bench.py:187-189
+            from .grid import dump_field
+            with open(args.dump, "w") as fh:
+                dump_field(grid, fh)
     sys.stdout.write(report(results, args.format))
     return 1 if any(r.verified == "no" for r in results) else 0
 
@@ -280,6 +284,7 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--reps", type=int, default=3)
     p.add_argument("--no-verify", action="store_true")
     p.add_argument("--format", choices=("csv", "json"), default="csv")
+    p.add_argument("--dump", default=None, help="write the final field here (the reference's text format)")
     p.set_defaults(func=cmd_bench)
     p = sub.add_parser("verify", help="oracle equivalence for one configuration")
     _add_config_flags(p)

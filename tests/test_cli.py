@@ -28,8 +28,18 @@ def test_report_format():
     assert '"mlups": "0.016"' in report([r], "json")
 
 
+def _need_reference():
+    """The CLI verifies against the reference package (baseline/_ref); skip where it is absent."""
+    from paper_0912_4506_b200.cli import ReferenceUnavailable, _import_reference, build_parser
+    try:
+        _import_reference(build_parser().parse_args(["verify"]))
+    except ReferenceUnavailable:
+        pytest.skip("reference package not installed (pip install --target baseline/_ref)")
+
+
 @pytest.mark.gpu
 def test_cli_bench_verify_dist_on_gpu():
+    _need_reference()
     from paper_0912_4506_b200.cli import cli_main
     out = io.StringIO()
     with redirect_stdout(out):
@@ -54,6 +64,7 @@ def test_cli_bench_verify_dist_on_gpu():
 def test_cli_compressed_and_float32_on_gpu():
     """--storage compressed (R/bench.py:114,147-150,199-201; reference test_bench.py:81-92)
     and --dtype float32, both verified against the reference package."""
+    _need_reference()
     from paper_0912_4506_b200.cli import cli_main
     out = io.StringIO()
     with redirect_stdout(out):
@@ -115,3 +126,25 @@ def _import_reference_no_default(args):
         _import_reference(args)
     finally:
         builtins.__import__ = real
+
+
+@pytest.mark.gpu
+def test_cli_dump_matches_oracle(O, tmp_path):
+    """`bench --dump` (R/bench.py:187-189): the field a GPU run leaves -- the
+    compressed pipeline included -- equals the oracle's, independent of the
+    reference package (checked here by the test, not by the CLI)."""
+    import numpy as np
+    from paper_0912_4506_b200 import load_field
+    from paper_0912_4506_b200.cli import cli_main
+    for storage in ("twogrid", "compressed"):
+        path = tmp_path / f"field_{storage}.txt"
+        with redirect_stdout(io.StringIO()):
+            assert cli_main(["bench", "--size", "16", "--variant", "pipeline", "--storage", storage,
+                             "--teams", "1", "--team-size", "2", "-T", "2", "--sweeps", "3", "--reps", "1",
+                             "--no-verify", "--dump", str(path)]) == 0
+        with open(path) as fh:
+            dims, field = load_field(fh)
+        levels = (3 + 1) * 4                          # warm-up sweep + 3 timed, U = 4 each
+        g = O.CGrid((16, 16, 16), O.BoxPattern("random", seed=42))
+        g.sweeps(levels)
+        assert np.array_equal(field[1:-1, 1:-1, 1:-1].view(np.uint64), g.interior().view(np.uint64)), storage
