@@ -13,6 +13,12 @@ for T in 2 4; do timeout 400 python bench.py --storage compressed --depth $T --n
 timeout 900 python -m pytest tests -m gpu -q > $D/gputests.log 2>&1
 python -c "import __graft_entry__ as g; g.smoke()" > $D/smoke.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $D/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > $D/ncu_launch.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:tb_kernel --launch-skip 2 -c 1 -o $D/ncu_full_c3_T4 python scripts/one_pass.py --n 1024 --depth 4 --passes 3 > $D/ncu_full_c3_T4.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:tb_kernel --launch-skip 2 -c 1 -o $D/ncu_full_c4_T4 python scripts/one_pass.py --n 1024 --nz 2048 --dtype f32 --depth 4 --passes 3 > $D/ncu_full_c4_T4.log 2>&1
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:tb_kernel --launch-skip 2 -c 1 -o $D/ncu_full_c3_T2 python scripts/one_pass.py --n 1024 --depth 2 --passes 3 > $D/ncu_full_c3_T2.log 2>&1
+# full captures go to /tmp on the box (reports of this kernel exceed gpurun's copy-back limit);
+# their summaries (details page, raw metrics, instruction mix) come back in $D
+mkdir -p /tmp/ncu_full
+for C in "c3_T4 --n 1024 --depth 4" "c4_T4 --n 1024 --nz 2048 --dtype f32 --depth 4" "c3_T2 --n 1024 --depth 2" "c3_T8 --n 1024 --depth 8"; do
+  set -- $C; N=$1; shift
+  timeout 600 ncu --set full --import-source on --clock-control none -k regex:tb_kernel --launch-skip 2 -c 1 -o /tmp/ncu_full/$N python scripts/one_pass.py "$@" --passes 3 > $D/ncu_full_$N.log 2>&1
+  python scripts/summarize_ncu.py full /tmp/ncu_full/$N.ncu-rep $D/ncu_full_$N >> $D/ncu_full_$N.log 2>&1
+  python scripts/ncu_step_mix.py /tmp/ncu_full/$N.ncu-rep 12 > $D/step_mix_$N.txt 2>&1
+done
