@@ -270,8 +270,13 @@ bool usable_rt(int T, int v) {
     }
 }
 
-int variant_for(int dtype, int T) {
+// `cells`: output cells of the pass (0 = large).  fp64 T=4 picks its shape by
+// size: 8x4/3 (15) on 1024^3-class passes (776-787 vs 749-757 GLUP/s), the
+// 12x3/2 hoisted shape (34) on smaller ones (512^3: 582 vs 511) -- its
+// 64x36 tiles balance better when a pass has few units.
+int variant_for(int dtype, int T, int64_t cells = 0) {
     int v = default_variant(dtype, T);
+    if (dtype == SP_F64 && T == 4 && cells > 0 && cells < (int64_t(1) << 28)) v = 34;
     if (g_variant_override >= 0 && g_variant_override < kNumVariants) v = g_variant_override;
     bool ok = dtype == SP_F64 ? usable_rt<double>(T, v) : usable_rt<float>(T, v);
     return ok ? v : 0;
@@ -813,7 +818,9 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
         const int64_t nxo = out_hi[2] - out_lo[2];
         if ((nxo + ox_pair - 1) / ox_pair == (nxo + a.ox - 1) / a.ox) a.ox = ox_pair;
     }
-    const int variant = peer ? kPeerVariant : (inplace ? inplace_variant_rt(dtype, T) : variant_for(dtype, T));
+    const int64_t out_cells = (out_hi[0] - out_lo[0]) * (out_hi[1] - out_lo[1]) * (out_hi[2] - out_lo[2]);
+    const int variant = peer ? kPeerVariant
+                             : (inplace ? inplace_variant_rt(dtype, T) : variant_for(dtype, T, out_cells));
     const int cl = kVariants[variant].cl;
     const int wy = kVariants[variant].by * kVariants[variant].py * cl;   // cluster footprint rows
     if (wy - 2 * T < 1) return fail(SP_ERR_SCHEDULE, "depth T=%d too deep for a %d-row footprint", T, wy);
