@@ -252,7 +252,10 @@ bool is_usable(int v) {
         case 57: return usable<R, T, 57>();
         case 58: return usable<R, T, 58>();
         case 59: return usable<R, T, 59>();
-        default: return usable<R, T, 60>();
+        case 60: return usable<R, T, 60>();
+        case 61: return usable<R, T, 61>();
+        case 62: return usable<R, T, 62>();
+        default: return usable<R, T, 63>();
     }
 }
 

@@ -126,8 +126,12 @@ constexpr Variant kVariants[] = {
     {8, 4, 3, 1, 8, 1, 1, 0, 1, 1, 1, 0, 8},   // 58: 15 in strips of 8
     {12, 3, 3, 1, 8, 1, 1, 0, 1, 1, 1, 0, 4},  // 59: 21 in strips of 4
     {8, 8, 2, 1, 8, 1, 0, 128, 1, 1, 1, 0, 4}, // 60: fp32: 8 in strips of 4
+    // fp32 with the 3-slot rotating queue (no queue moves)
+    {8, 8, 3, 1, 8, 1, 0, 128},              // 61: 8x8/3
+    {8, 6, 3, 1, 8, 1, 0, 128},              // 62: 8x6/3 (64x48 footprint)
+    {8, 6, 3, 1, 8, 1, 1, 128},              // 63: 62 with the split barrier
 };
-constexpr int kNumVariants = 61;
+constexpr int kNumVariants = 64;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -162,6 +166,7 @@ constexpr bool compiled() {
     if (V >= 53 && V <= 55) return sizeof(R) == 8 && T >= 3 && T <= 4;
     if (V >= 56 && V <= 59) return sizeof(R) == 8 && T >= 2 && T <= 4;
     if (V == 60) return sizeof(R) == 4 && T >= 2 && T <= 4;
+    if (V >= 61 && V <= 63) return sizeof(R) == 4 && T >= 3 && T <= 4;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -344,7 +349,10 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 57: return launch_tb_t<R, T, 57>(src, L, a, grid, s);
         case 58: return launch_tb_t<R, T, 58>(src, L, a, grid, s);
         case 59: return launch_tb_t<R, T, 59>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 60>(src, L, a, grid, s);
+        case 60: return launch_tb_t<R, T, 60>(src, L, a, grid, s);
+        case 61: return launch_tb_t<R, T, 61>(src, L, a, grid, s);
+        case 62: return launch_tb_t<R, T, 62>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 63>(src, L, a, grid, s);
     }
 }
 
