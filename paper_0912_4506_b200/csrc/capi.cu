@@ -164,16 +164,18 @@ thread_local int g_variant_override = -1;
 // Default variant per (dtype, T), from same-box B200 sweeps
 // (profiles/r01_tuning.md, "split barrier" table).
 int default_variant(int dtype, int T) {
+    // tq_kernel (tq.cuh) keeps the z-queue in tensor memory: "tq" = v[p-1] there, "FQ" = both
+    // older planes there (no queue registers).  Same-box sweeps: profiles/r02_tuning.md.
     if (dtype == SP_F64) {
         switch (T) {
             case 1: return 5;    // 16x2/3, ring 6
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
-            case 3: return 21;   // 12x3/3, split, running output pointer
-            case 4: return 15;   // 8x4/3, split, running output pointer (after the branch-free FAST loop:
-                                 // 776-787 vs 749-757 for 34, 12x3/2 hoisted)
-            case 5: return 27;   // 8x4, level 0 re-read from the ring (slots 4), split
-            case 6: return 48;   // level split over two CTAs, 12x3 hoisted, role-swapped 2-slot queue each
-            case 8: return 48;   // the same (4 levels per CTA); +3-5 % over 40
+            case 3: return 89;   // tq 16x3 hoisted: 772-814 vs 748-786 for 21 (12x3/3)
+            case 4: return 123;  // FQ 12x5 (64x60 footprint): 868-874; FQ 16x4 840, 15 (8x4/3) 745-768
+            case 5: return 110;  // FQ 8x6: 809-845 vs 606 for 27
+            case 6: return 112;  // FQ 8x4: 677-681 vs 620 for the level split 48
+            case 7: return 112;  // FQ 8x4 (the register-queue shapes spill: 126)
+            case 8: return 112;  // FQ 8x4: 543 vs 523 for the level split 48
             default: return 12;  // 8x4/2, split
         }
     }
@@ -181,10 +183,11 @@ int default_variant(int dtype, int T) {
         case 1: return 14;       // 16x2/3
         case 2: return 16;       // 8x8/2, two CTAs per SM, split
         case 3: return 37;       // 12x6/2, running output pointer, hoisted xy sums (+3.5 % over 22)
-        case 4: return 8;        // 8x8/2, running output pointer
-        case 5: return 11;       // 16x2/2, split
-        case 6: return 51;       // level split over two CTAs, 16x4/2 hoisted each (64x64): 1158 vs 889
-        case 8: return 52;       // level split over two CTAs, 8x8 role-swapped (64x64): 1279 vs 860
+        case 4: return 92;       // tq 12x6 (64x72 footprint): 1782-1886 vs 1527-1536 for 8 (8x8/2)
+        case 5: return 92;       // tq 12x6: 1659-1733 vs 960 for 11
+        case 6: return 121;      // FQ 16x4 (64x64): 1558-1568 vs 1151 for the level split 51
+        case 7: return 121;      // FQ 16x4: 1464-1486 vs 829 for 2
+        case 8: return 111;      // FQ 8x8 (64x64): 1522-1556 vs 1170 for the level split 52
         default: return 2;       // 8x4/2
     }
 }
@@ -255,7 +258,71 @@ bool is_usable(int v) {
         case 60: return usable<R, T, 60>();
         case 61: return usable<R, T, 61>();
         case 62: return usable<R, T, 62>();
-        default: return usable<R, T, 63>();
+        case 63: return usable<R, T, 63>();
+        case 64: return usable<R, T, 64>();
+        case 65: return usable<R, T, 65>();
+        case 66: return usable<R, T, 66>();
+        case 67: return usable<R, T, 67>();
+        case 68: return usable<R, T, 68>();
+        case 69: return usable<R, T, 69>();
+        case 70: return usable<R, T, 70>();
+        case 71: return usable<R, T, 71>();
+        case 72: return usable<R, T, 72>();
+        case 73: return usable<R, T, 73>();
+        case 74: return usable<R, T, 74>();
+        case 75: return usable<R, T, 75>();
+        case 76: return usable<R, T, 76>();
+        case 77: return usable<R, T, 77>();
+        case 78: return usable<R, T, 78>();
+        case 79: return usable<R, T, 79>();
+        case 80: return usable<R, T, 80>();
+        case 81: return usable<R, T, 81>();
+        case 82: return usable<R, T, 82>();
+        case 83: return usable<R, T, 83>();
+        case 84: return usable<R, T, 84>();
+        case 85: return usable<R, T, 85>();
+        case 86: return usable<R, T, 86>();
+        case 87: return usable<R, T, 87>();
+        case 88: return usable<R, T, 88>();
+        case 89: return usable<R, T, 89>();
+        case 90: return usable<R, T, 90>();
+        case 91: return usable<R, T, 91>();
+        case 92: return usable<R, T, 92>();
+        case 93: return usable<R, T, 93>();
+        case 94: return usable<R, T, 94>();
+        case 95: return usable<R, T, 95>();
+        case 96: return usable<R, T, 96>();
+        case 97: return usable<R, T, 97>();
+        case 98: return usable<R, T, 98>();
+        case 99: return usable<R, T, 99>();
+        case 100: return usable<R, T, 100>();
+        case 101: return usable<R, T, 101>();
+        case 102: return usable<R, T, 102>();
+        case 103: return usable<R, T, 103>();
+        case 104: return usable<R, T, 104>();
+        case 105: return usable<R, T, 105>();
+        case 106: return usable<R, T, 106>();
+        case 107: return usable<R, T, 107>();
+        case 108: return usable<R, T, 108>();
+        case 109: return usable<R, T, 109>();
+        case 110: return usable<R, T, 110>();
+        case 111: return usable<R, T, 111>();
+        case 112: return usable<R, T, 112>();
+        case 113: return usable<R, T, 113>();
+        case 114: return usable<R, T, 114>();
+        case 115: return usable<R, T, 115>();
+        case 116: return usable<R, T, 116>();
+        case 117: return usable<R, T, 117>();
+        case 118: return usable<R, T, 118>();
+        case 119: return usable<R, T, 119>();
+        case 120: return usable<R, T, 120>();
+        case 121: return usable<R, T, 121>();
+        case 122: return usable<R, T, 122>();
+        case 123: return usable<R, T, 123>();
+        case 124: return usable<R, T, 124>();
+        case 125: return usable<R, T, 125>();
+        case 126: return usable<R, T, 126>();
+        default: return usable<R, T, 127>();
     }
 }
 
@@ -273,13 +340,12 @@ bool usable_rt(int T, int v) {
     }
 }
 
-// `cells`: output cells of the pass (0 = large).  fp64 T=4 picks its shape by
-// size: 8x4/3 (15) on 1024^3-class passes (776-787 vs 749-757 GLUP/s), the
-// 12x3/2 hoisted shape (34) on smaller ones (512^3: 582 vs 511) -- its
-// 64x36 tiles balance better when a pass has few units.
+// `cells`: output cells of the pass (unused since the tensor-memory kernels: round 2's
+// size-dependent fp64 T=4 pick -- 12x3/2 hoisted below 2^28 cells -- lost to FQ 12x5 at
+// 512^3 too, 701 vs 580 GLUP/s).
 int variant_for(int dtype, int T, int64_t cells = 0) {
     int v = default_variant(dtype, T);
-    if (dtype == SP_F64 && T == 4 && cells > 0 && cells < (int64_t(1) << 28)) v = 34;
+    (void)cells;
     if (g_variant_override >= 0 && g_variant_override < kNumVariants) v = g_variant_override;
     bool ok = dtype == SP_F64 ? usable_rt<double>(T, v) : usable_rt<float>(T, v);
     return ok ? v : 0;
@@ -614,9 +680,13 @@ int sp_describe_variant(int dtype, int T, char* buf, int buflen) {
     const int v = variant_for(dtype, T);
     const Variant& k = kVariants[v];
     if (buf && buflen > 0) {
-        const char* q = k.slots == 1 ? "v[p-1] from shared memory"
+        const char* q = k.tq && k.fq ? "z-queue (v[p-1], v[p]) of every level in tensor memory (tcgen05.ld/st)"
+                      : k.tq ? "v[p] in registers by step parity, v[p-1] in tensor memory (tcgen05.ld/st)"
+                      : k.slots == 1 ? "v[p-1] from shared memory"
                       : k.slots == 2 ? "2-slot register z-queue"
                       : k.slots == 3 ? "3-slot rotating register z-queue"
+                      : k.slots == 6 ? "level 0 re-read from the ring, 3-slot rotating queues above"
+                      : k.slots == 5 ? "role-swapped 2-slot register z-queue"
                                      : "level 0 re-read from the ring, 2-slot queue above";
         snprintf(buf, (size_t)buflen,
                  "variant %d: %d warps x %d rows (64x%d footprint), %s, %d CTA/SM, %s step sync%s%s%s",

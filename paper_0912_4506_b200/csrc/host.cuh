@@ -49,6 +49,9 @@ struct Variant {
     int lag = 1;                     // 2: lag-2 z-wavefront (tb2_kernel, wave2.cuh)
     int hoist = 0;                   // xy-sum placement in the step (see tb_kernel HOIST)
     int ys = 0;                      // > 0: y strips of this many tiles (saved rows, no bottom halo)
+    int tq = 0;                      // 1: tq_kernel (tq.cuh): v[p-1] of every level in tensor memory
+    int sg = 0;                      // tq_kernel: columns per tcgen05.st (0: one wide store per level)
+    int fq = 0;                      // tq_kernel: 1 = v[p] in tensor memory too (no z-queue registers)
 };
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
@@ -130,8 +133,77 @@ constexpr Variant kVariants[] = {
     {8, 8, 3, 1, 8, 1, 0, 128},              // 61: 8x8/3
     {8, 6, 3, 1, 8, 1, 0, 128},              // 62: 8x6/3 (64x48 footprint)
     {8, 6, 3, 1, 8, 1, 1, 128},              // 63: 62 with the split barrier
+    // slots 6: level 0 re-read from the TMA ring every step (never in registers across
+    // steps), 3-slot rotating queues above: no queue moves, one level less of register state
+    {12, 3, 6, 1, 8, 1, 1},                  // 64: 12x3, split
+    {12, 3, 6, 1, 8, 1, 1, 0, 1, 1, 1, 3},   // 65: 64 hoisted
+    {12, 3, 6, 1, 8, 1, 1, 0, 1, 1, 1, 1},   // 66: 64, level 1's sums before the TMA wait
+    {8, 4, 6, 1, 8, 1, 1},                   // 67: 8x4, split
+    {8, 4, 6, 1, 8, 1, 1, 0, 1, 1, 1, 3},    // 68: 67 hoisted
+    {16, 2, 6, 1, 8, 1, 1},                  // 69: 16x2 (<= 128 registers)
+    {8, 4, 6, 2, 8, 0, 1, 80},               // 70: 9's shape (two CTAs per SM)
+    {8, 8, 6, 1, 8, 1, 0, 128},              // 71: fp32 8x8
+    {12, 6, 6, 1, 8, 1, 0, 128, 1, 1, 1, 3}, // 72: fp32 12x6 hoisted
+    {12, 3, 6, 1, 8, 1, 1, 0, 1, 2, 1, 3},   // 73: level split, 65 per CTA
+    {16, 3, 6, 1, 8, 1, 1},                  // 74: 16x3 (64x48 footprint, <= 128 registers)
+    // tq_kernel: v[p-1] of every level in tensor memory, taller patches (slots/minb/rstore/split fixed)
+    {8, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},   // 75: 8x4 (64x32)
+    {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},   // 76: 8x6 (64x48)
+    {8, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},   // 77: 8x8 (64x64)
+    {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1},   // 78: 76 hoisted
+    {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1},   // 79: 76, level 1's sums before the TMA wait
+    {12, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 80: 12x4 (64x48, <= 168 registers)
+    {8, 12, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 81: fp32 8x12 (64x96)
+    {8, 16, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 82: fp32 8x16 (64x128)
+    {8, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1},   // 83: 77 hoisted
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 84: 16x3 (64x48, <= 128 registers: four warps per scheduler)
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 85: 16x4 (64x64, <= 128 registers)
+    {16, 2, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 86: 16x2 (64x32, <= 128 registers)
+    {8, 5, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},   // 87: 8x5 (64x40)
+    {12, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 88: 12x3 (64x36, <= 168 registers)
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1},  // 89: 84 hoisted
+    {16, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 90: fp32 16x6 (64x96, <= 128 registers)
+    {16, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 91: fp32 16x8 (64x128, <= 128 registers)
+    {12, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 92: fp32 12x6 (64x72, <= 168 registers)
+    {12, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1},  // 93: fp32 12x8 (64x96)
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1},  // 94: 85 hoisted
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1},  // 95: 85, level 1's sums before the TMA wait
+    {12, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1},  // 96: 92 hoisted
+    {12, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1},  // 97: 88 hoisted
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1},  // 98: 84, level 1's sums before the TMA wait
+    {12, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1},  // 99: 88, level 1's sums before the TMA wait
+    // tq_kernel with narrow TMEM stores (no register gather moves)
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1, 2},  // 100: 89, one store per fp64 value
+    {12, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2},  // 101: 88
+    {12, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2},  // 102: 92 (fp32: one store per x pair)
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2},  // 103: 85
+    {8, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2},   // 104: 75
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2},  // 105: 84
+    {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2},   // 106: 76
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1, 4},  // 107: 89, one store per x pair
+    {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 3, 0, 1, 2},   // 108: 78
+    {12, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2},  // 109: 80
+    // tq_kernel with both older planes of every level in tensor memory (FQ)
+    {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},   // 110: 8x6 (64x48)
+    {8, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},   // 111: 8x8 (64x64)
+    {8, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},   // 112: 8x4 (64x32)
+    {12, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 113: 12x4 (64x48)
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 114: 16x3 (64x48)
+    {8, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 0, 1},   // 115: 111 with wide stores
+    {12, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 116: 12x6 (64x72)
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 117: 16x4 (64x64)
+    {8, 12, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 118: fp32 8x12 (64x96)
+    {12, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 119: fp32 12x8 (64x96)
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},  // 120: 117, level 1's sums before the TMA wait
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 4, 1},  // 121: 117, one store per x pair
+    {16, 5, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 122: 16x5 (64x80)
+    {12, 5, 2, 1, 8, 1, 1, 0, 1, 1, 1, 0, 0, 1, 2, 1},  // 123: 12x5 (64x60)
+    {8, 8, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},   // 124: 111, level 1's sums before the TMA wait
+    {12, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},  // 125: 116, level 1's sums before the TMA wait
+    {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},   // 126: 110, level 1's sums before the TMA wait
+    {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},  // 127: 114, level 1's sums before the TMA wait
 };
-constexpr int kNumVariants = 64;
+constexpr int kNumVariants = 128;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -167,6 +239,22 @@ constexpr bool compiled() {
     if (V >= 56 && V <= 59) return sizeof(R) == 8 && T >= 2 && T <= 4;
     if (V == 60) return sizeof(R) == 4 && T >= 2 && T <= 4;
     if (V >= 61 && V <= 63) return sizeof(R) == 4 && T >= 3 && T <= 4;
+    // slots 6 (level 0 from the ring): measured within 3 % of the defaults, superseded by
+    // tq_kernel; 64/65/72 stay built as the tested record (profiles/r02_tuning.md)
+    if (V == 64 || V == 65) return sizeof(R) == 8 && T >= 3 && T <= 4;
+    if (V == 72) return sizeof(R) == 4 && T >= 3 && T <= 4;
+    if (V >= 64 && V <= 74) return false;
+    // tq_kernel shapes still built (the others of 75..109 were measured and lost:
+    // profiles/r02_tuning.md)
+    if (V == 88) return T >= 2;                                        // 12x3
+    if (V == 85) return T >= 2 && (sizeof(R) == 4 || T <= 3);         // 16x4
+    if (V == 89) return T >= 2 && T <= 4;                             // 16x3 hoisted
+    if (V == 80 || V == 92) return sizeof(R) == 4 && T >= 2;          // fp32 12x4, 12x6
+    if (V == 96) return sizeof(R) == 4 && T >= 2 && T <= 6;           // fp32 12x6 hoisted
+    if (V >= 75 && V <= 109) return false;
+    if (V >= 110 && V <= 117) return T >= 2;
+    if (V == 118 || V == 119) return sizeof(R) == 4 && T >= 2;
+    if (V >= 120 && V <= 127) return T >= 2;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -182,6 +270,9 @@ constexpr bool usable() {
     constexpr Variant v = kVariants[V];
     if constexpr (!compiled<R, T, V>()) {
         return false;
+    } else if constexpr (v.tq) {
+        if constexpr (T >= 2 && T * v.py <= 64) return sp::PlanQ<R, T, v.by, v.py, v.ring, v.fq>::FITS;
+        else return false;
     } else if constexpr (v.lag == 2) {
         return T >= 2 && sp::Plan2<R, T, v.by, v.py, v.minb, v.ring>::FITS;
     } else {
@@ -198,12 +289,16 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
     } else {
         constexpr Variant v = kVariants[V];
-        static_assert(v.lag == 1 || (!PEER && !INPL), "lag-2 variants: two-grid passes only");
-        using Pl = std::conditional_t<v.lag == 2, sp::Plan2<R, T, v.by, v.py, v.minb, v.ring>,
-                                      sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls, v.ys>>;
+        static_assert((v.lag == 1 && !v.tq) || (!PEER && !INPL), "lag-2 / tensor-memory variants: two-grid passes only");
+        constexpr bool two_arg = v.lag == 2 || v.tq;   // kernels without the saved-rows tensor map
+        using Pl = std::conditional_t<
+            v.tq != 0, sp::PlanQ<R, T, v.by, v.py, v.ring, v.fq>,
+            std::conditional_t<v.lag == 2, sp::Plan2<R, T, v.by, v.py, v.minb, v.ring>,
+                               sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls, v.ys>>>;
         auto kern = [] {
             constexpr Variant w = kVariants[V];
-            if constexpr (w.lag == 2) return sp::tb2_kernel<R, T, w.by, w.py, w.minb, w.ring>;
+            if constexpr (w.tq) return sp::tq_kernel<R, T, w.by, w.py, w.ring, w.hoist, w.sg, w.fq>;
+            else if constexpr (w.lag == 2) return sp::tb2_kernel<R, T, w.by, w.py, w.minb, w.ring>;
             else return sp::tb_kernel<R, T, w.by, w.py, w.slots, w.minb, w.ring, w.rstore, w.split, PEER, w.cl,
                                       w.ls, INPL, w.hoist, w.ys>;
         }();
@@ -231,7 +326,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
                          SP_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(SP_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
         CUtensorMap map_sv = map;   // y strips: the saved rows [CTA * steps][T-1][WX]
-        if constexpr (v.ys > 0 && v.lag == 1) {
+        if constexpr (v.ys > 0 && v.lag == 1 && !v.tq) {
             constexpr int NLV = T / v.ls - 1;
             if (!a.ysave || a.sv_steps < 1) return fail(SP_ERR_ARG, "y-strip pass without its scratch");
             cuuint64_t sdim[3] = {(cuuint64_t)sp::WX, (cuuint64_t)NLV, (cuuint64_t)grid * (cuuint64_t)a.sv_steps};
@@ -272,10 +367,10 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
             }
             const int clusters = (int)std::min<int64_t>(a.units, (int64_t)(nc - 1));
             cfg.gridDim = dim3(clusters * csize, 1, 1);
-            if constexpr (v.lag == 2) SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a));
+            if constexpr (two_arg) SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, a));
             else SP_CUDA(cudaLaunchKernelEx(&cfg, kern, map, map_sv, a));
         } else {
-            if constexpr (v.lag == 2) kern<<<grid, Pl::NT, smem, stream>>>(map, a);
+            if constexpr (two_arg) kern<<<grid, Pl::NT, smem, stream>>>(map, a);
             else kern<<<grid, Pl::NT, smem, stream>>>(map, map_sv, a);
         }
         g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -352,7 +447,71 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 60: return launch_tb_t<R, T, 60>(src, L, a, grid, s);
         case 61: return launch_tb_t<R, T, 61>(src, L, a, grid, s);
         case 62: return launch_tb_t<R, T, 62>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 63>(src, L, a, grid, s);
+        case 63: return launch_tb_t<R, T, 63>(src, L, a, grid, s);
+        case 64: return launch_tb_t<R, T, 64>(src, L, a, grid, s);
+        case 65: return launch_tb_t<R, T, 65>(src, L, a, grid, s);
+        case 66: return launch_tb_t<R, T, 66>(src, L, a, grid, s);
+        case 67: return launch_tb_t<R, T, 67>(src, L, a, grid, s);
+        case 68: return launch_tb_t<R, T, 68>(src, L, a, grid, s);
+        case 69: return launch_tb_t<R, T, 69>(src, L, a, grid, s);
+        case 70: return launch_tb_t<R, T, 70>(src, L, a, grid, s);
+        case 71: return launch_tb_t<R, T, 71>(src, L, a, grid, s);
+        case 72: return launch_tb_t<R, T, 72>(src, L, a, grid, s);
+        case 73: return launch_tb_t<R, T, 73>(src, L, a, grid, s);
+        case 74: return launch_tb_t<R, T, 74>(src, L, a, grid, s);
+        case 75: return launch_tb_t<R, T, 75>(src, L, a, grid, s);
+        case 76: return launch_tb_t<R, T, 76>(src, L, a, grid, s);
+        case 77: return launch_tb_t<R, T, 77>(src, L, a, grid, s);
+        case 78: return launch_tb_t<R, T, 78>(src, L, a, grid, s);
+        case 79: return launch_tb_t<R, T, 79>(src, L, a, grid, s);
+        case 80: return launch_tb_t<R, T, 80>(src, L, a, grid, s);
+        case 81: return launch_tb_t<R, T, 81>(src, L, a, grid, s);
+        case 82: return launch_tb_t<R, T, 82>(src, L, a, grid, s);
+        case 83: return launch_tb_t<R, T, 83>(src, L, a, grid, s);
+        case 84: return launch_tb_t<R, T, 84>(src, L, a, grid, s);
+        case 85: return launch_tb_t<R, T, 85>(src, L, a, grid, s);
+        case 86: return launch_tb_t<R, T, 86>(src, L, a, grid, s);
+        case 87: return launch_tb_t<R, T, 87>(src, L, a, grid, s);
+        case 88: return launch_tb_t<R, T, 88>(src, L, a, grid, s);
+        case 89: return launch_tb_t<R, T, 89>(src, L, a, grid, s);
+        case 90: return launch_tb_t<R, T, 90>(src, L, a, grid, s);
+        case 91: return launch_tb_t<R, T, 91>(src, L, a, grid, s);
+        case 92: return launch_tb_t<R, T, 92>(src, L, a, grid, s);
+        case 93: return launch_tb_t<R, T, 93>(src, L, a, grid, s);
+        case 94: return launch_tb_t<R, T, 94>(src, L, a, grid, s);
+        case 95: return launch_tb_t<R, T, 95>(src, L, a, grid, s);
+        case 96: return launch_tb_t<R, T, 96>(src, L, a, grid, s);
+        case 97: return launch_tb_t<R, T, 97>(src, L, a, grid, s);
+        case 98: return launch_tb_t<R, T, 98>(src, L, a, grid, s);
+        case 99: return launch_tb_t<R, T, 99>(src, L, a, grid, s);
+        case 100: return launch_tb_t<R, T, 100>(src, L, a, grid, s);
+        case 101: return launch_tb_t<R, T, 101>(src, L, a, grid, s);
+        case 102: return launch_tb_t<R, T, 102>(src, L, a, grid, s);
+        case 103: return launch_tb_t<R, T, 103>(src, L, a, grid, s);
+        case 104: return launch_tb_t<R, T, 104>(src, L, a, grid, s);
+        case 105: return launch_tb_t<R, T, 105>(src, L, a, grid, s);
+        case 106: return launch_tb_t<R, T, 106>(src, L, a, grid, s);
+        case 107: return launch_tb_t<R, T, 107>(src, L, a, grid, s);
+        case 108: return launch_tb_t<R, T, 108>(src, L, a, grid, s);
+        case 109: return launch_tb_t<R, T, 109>(src, L, a, grid, s);
+        case 110: return launch_tb_t<R, T, 110>(src, L, a, grid, s);
+        case 111: return launch_tb_t<R, T, 111>(src, L, a, grid, s);
+        case 112: return launch_tb_t<R, T, 112>(src, L, a, grid, s);
+        case 113: return launch_tb_t<R, T, 113>(src, L, a, grid, s);
+        case 114: return launch_tb_t<R, T, 114>(src, L, a, grid, s);
+        case 115: return launch_tb_t<R, T, 115>(src, L, a, grid, s);
+        case 116: return launch_tb_t<R, T, 116>(src, L, a, grid, s);
+        case 117: return launch_tb_t<R, T, 117>(src, L, a, grid, s);
+        case 118: return launch_tb_t<R, T, 118>(src, L, a, grid, s);
+        case 119: return launch_tb_t<R, T, 119>(src, L, a, grid, s);
+        case 120: return launch_tb_t<R, T, 120>(src, L, a, grid, s);
+        case 121: return launch_tb_t<R, T, 121>(src, L, a, grid, s);
+        case 122: return launch_tb_t<R, T, 122>(src, L, a, grid, s);
+        case 123: return launch_tb_t<R, T, 123>(src, L, a, grid, s);
+        case 124: return launch_tb_t<R, T, 124>(src, L, a, grid, s);
+        case 125: return launch_tb_t<R, T, 125>(src, L, a, grid, s);
+        case 126: return launch_tb_t<R, T, 126>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 127>(src, L, a, grid, s);
     }
 }
 

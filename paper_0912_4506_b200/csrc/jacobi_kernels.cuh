@@ -381,7 +381,7 @@ struct Plan {
     static constexpr int NBUF = DB ? 2 : 1;
     static constexpr int RING_FIT = (BUDGET - NBUF * NL * PLANE_BYTES) / (RPLANE_BYTES + SV_BYTES);
     static constexpr int RING = RING_FIT > RCAP ? RCAP : RING_FIT;
-    static constexpr int MIN_RING = SLOTS == 1 ? 4 : 3;
+    static constexpr int MIN_RING = (SLOTS == 1 || SLOTS == 6) ? 4 : 3;
     static constexpr bool FITS = RING >= MIN_RING && CL * WY - 2 * T >= 1 && (SLOTS != 1 || DB) &&
                                  (CL == 1 || (DB && SLOTS != 1 && T >= 2)) &&
                                  (YS == 0 || (DB && T >= 2 && CL == 1 && LS == 1));
@@ -426,8 +426,16 @@ __global__ void __launch_bounds__(32 * BY, MINB)
     // v[p-1]; only the new plane moves into the dead v[p-1] slot -- one
     // register move per value instead of two.
     constexpr bool RSW = SLOTS == 5;
-    constexpr int QS = (L0C || RSW) ? 2 : SLOTS;
-    static_assert(SLOTS >= 1 && SLOTS <= 5, "z-queue slots");
+    // SLOTS = 6: level 0 is never held in registers across steps -- its three
+    // planes (q-2, q-1, q) are re-read from the TMA ring every step (the ring
+    // keeps them anyway) -- and levels >= 1 use the 3-slot rotating queue: no
+    // queue moves and one level less of register state (12x3 at T=4 fits 168
+    // registers, i.e. three warps per scheduler, without the 2-slot shift).
+    constexpr bool L0R = SLOTS == 6;
+    constexpr int QS = (L0C || RSW) ? 2 : (L0R ? 3 : SLOTS);
+    // the ring slot of plane q-2 is still read in step k (SLOTS 1 and 6)
+    constexpr bool LATE = QS == 1 || L0R;
+    static_assert(SLOTS >= 1 && SLOTS <= 6, "z-queue slots");
     static_assert(!INPL || (CL == 1 && LS == 1 && !PEER), "in-place passes: single-CTA variants");
     static_assert(LS == 1 || (T % LS == 0 && CL == 1 && !PEER && QS != 1),
                   "level split: depth a multiple of the cluster size");
@@ -574,7 +582,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
         if constexpr (YS > 0)
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_sv)) : "memory");
         // the slot released after step k is k-1 (k-2 with SLOTS == 1): prime the rest
-        for (int i = 0; i < RING_N - (QS == 1 ? 2 : 1); ++i) produce(i);
+        for (int i = 0; i < RING_N - (LATE ? 2 : 1); ++i) produce(i);
     }
 
     if constexpr (INPL) {   // the first unit's dependencies (see the end of the unit loop)
@@ -707,8 +715,20 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                         M0[C0][j][1] = r.y;
                     }
                 }
+                // L0R: level 0 at planes q-1 (v[p]), q-2 (v[p-1]) and q (new), transients of this step
+                R L0c[PY][PX], L0m[PY][PX], L0n[PY][PX];
+                if constexpr (L0R) {
+                    const R* Lc = ring + pslot * RPLANE + HR * WX;
+    #pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        V2 r = *reinterpret_cast<const V2*>(Lc + (cy + j) * WX + cx);
+                        L0c[j][0] = r.x;
+                        L0c[j][1] = r.y;
+                    }
+                }
                 auto qcur = [&](int t) __attribute__((always_inline)) -> const R(&)[PY][PX] {   // level t's v[p]
                     if constexpr (L0C) return t == 0 ? M0[C0] : Q[F1][t];
+                    else if constexpr (L0R) return t == 0 ? L0c : Q[F1][t];
                     else return Q[F1][t];
                 };
 
@@ -781,7 +801,8 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                 // new planes of every level this step (SLOTS == 3: aliases of Q[F2])
                 R Nt[QS == 2 ? D : 1][PY][PX];
                 auto newv = [&](int t) __attribute__((always_inline)) -> R(&)[PY][PX] {
-                    if constexpr (QS != 2) return Q[F2][t];
+                    if constexpr (L0R) return t == 0 ? L0n : Q[F2][t];
+                    else if constexpr (QS != 2) return Q[F2][t];
                     else return Nt[t];
                 };
                 // QS == 1: v[p-1] of level t-1, re-read from shared memory
@@ -811,8 +832,20 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     if constexpr (P::DB) {
                         if (t == 1 ? !(HOIST & 1) : !(HOIST & 2)) xy_sums(t);
                     }
+                    if constexpr (L0R) {
+                        if (t == 1) {   // level 0's v[p-1]: plane q-2, still in the ring
+                            const R* Lm = ring + pslot2 * RPLANE + HR * WX;
+    #pragma unroll
+                            for (int j = 0; j < PY; ++j) {
+                                V2 r = *reinterpret_cast<const V2*>(Lm + (cy + j) * WX + cx);
+                                L0m[j][0] = r.x;
+                                L0m[j][1] = r.y;
+                            }
+                        }
+                    }
                     const R(&mm)[PY][PX] = *([&]() -> const R(*)[PY][PX] {
                         if constexpr (QS == 1) return &mv;
+                        else if constexpr (L0R) return t == 1 ? &L0m : &Q[F0][t - 1];
                         else if constexpr (L0C) return t == 1 ? &M0[M0I] : &Q[F0][t - 1];
                         else return &Q[F0][t - 1];
                     }());
@@ -871,7 +904,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                             // ring slot last read in step k-1: plane k-2 (k-3 with SLOTS == 1,
                             // which re-reads v[p-1] from slot k-2 at the start of a step)
-                            produce(QS == 1 ? (gstep + RING_N - 3) % RING_N : pslot2);
+                            produce(LATE ? (gstep + RING_N - 3) % RING_N : pslot2);
                         }
                     }
                     // HOIST bit 1: every deeper level's xy sums at once, right after step
@@ -975,7 +1008,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
                     // ring slot pslot (pslot2 with SLOTS == 1) was last read this step
                     if (threadIdx.x == 0) {
                         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                        produce(QS == 1 ? pslot2 : pslot);
+                        produce(LATE ? pslot2 : pslot);
                     }
                 }
                 ++gstep;
@@ -1035,6 +1068,7 @@ __global__ void __launch_bounds__(32 * BY, MINB)
 }
 
 #include "wave2.cuh"   // tb2_kernel: the lag-2 z-wavefront form of K2
+#include "tq.cuh"      // tq_kernel: K2 with the z-queue's older plane in tensor memory
 
 // ---- K1: single-level streaming sweep ---------------------------------------
 //

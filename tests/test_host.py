@@ -184,12 +184,12 @@ def test_describe_variant_defaults(sp):
     N = sp._native
     d = {(dt, T): N.describe_variant(dt, T) for dt in (N.SP_F64, N.SP_F32) for T in range(1, 9)}
     assert "2 CTA/SM" in d[(N.SP_F64, 2)] and "8 warps x 4 rows" in d[(N.SP_F64, 2)]
-    assert "12 warps x 3 rows" in d[(N.SP_F64, 3)]
-    assert "level split over a 2-CTA cluster" in d[(N.SP_F64, 8)]
-    assert "level split" in d[(N.SP_F64, 6)]
-    assert "level split" in d[(N.SP_F32, 8)] and "64x64 footprint" in d[(N.SP_F32, 8)]
-    assert "8 warps x 4 rows" in d[(N.SP_F64, 4)] and "3-slot" in d[(N.SP_F64, 4)]
-    assert "level split" not in d[(N.SP_F32, 4)]
+    assert "16 warps x 3 rows" in d[(N.SP_F64, 3)] and "tensor memory" in d[(N.SP_F64, 3)]
+    assert "12 warps x 5 rows" in d[(N.SP_F64, 4)] and "z-queue (v[p-1], v[p])" in d[(N.SP_F64, 4)]
+    assert "12 warps x 6 rows" in d[(N.SP_F32, 4)] and "tensor memory" in d[(N.SP_F32, 4)]
+    for T in range(5, 9):
+        assert "tensor memory" in d[(N.SP_F64, T)] and "tensor memory" in d[(N.SP_F32, T)]
+    assert "64x64 footprint" in d[(N.SP_F32, 8)]
     with pytest.raises(ValueError):
         N.describe_variant(N.SP_F64, 9)
 
