@@ -611,7 +611,7 @@ def verify_result(args, torch, dist, rank, world, cuda, grid, runners, passes, g
     -- slab digests summed mod 2^64 at N>1 -- with the oracle's golden digest
     for this global grid (tests/golden/big_digests.json, written by the pinned
     C oracle).  The CPU test engine hands the gathered field to HOOKS."""
-    if args.storage != "twogrid" or not (cuda or "verify" in HOOKS):
+    if not (cuda or "verify" in HOOKS):
         return None
     want = None
     if cuda:

@@ -171,7 +171,8 @@ int default_variant(int dtype, int T) {
             case 1: return 5;    // 16x2/3, ring 6
             case 2: return 9;    // 8x4/2, two CTAs per SM, split
             case 3: return 89;   // tq 16x3 hoisted: 772-814 vs 748-786 for 21 (12x3/3)
-            case 4: return 123;  // FQ 12x5 (64x60 footprint): 868-874; FQ 16x4 840, 15 (8x4/3) 745-768
+            case 4: return 130;  // FQ 12x5 (64x60 footprint), early level-1 sums + late v[p] loads: 916-921;
+                                 // plain FQ 12x5 (123) 884-904, FQ 16x4 876-882, 15 (8x4/3) 745-768 (box-dependent)
             case 5: return 110;  // FQ 8x6: 809-845 vs 606 for 27
             case 6: return 112;  // FQ 8x4: 677-681 vs 620 for the level split 48
             case 7: return 112;  // FQ 8x4 (the register-queue shapes spill: 126)
@@ -322,7 +323,11 @@ bool is_usable(int v) {
         case 124: return usable<R, T, 124>();
         case 125: return usable<R, T, 125>();
         case 126: return usable<R, T, 126>();
-        default: return usable<R, T, 127>();
+        case 127: return usable<R, T, 127>();
+        case 128: return usable<R, T, 128>();
+        case 129: return usable<R, T, 129>();
+        case 130: return usable<R, T, 130>();
+        default: return usable<R, T, 131>();
     }
 }
 

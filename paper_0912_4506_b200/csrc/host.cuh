@@ -202,8 +202,13 @@ constexpr Variant kVariants[] = {
     {12, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},  // 125: 116, level 1's sums before the TMA wait
     {8, 6, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},   // 126: 110, level 1's sums before the TMA wait
     {16, 3, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},  // 127: 114, level 1's sums before the TMA wait
+    // HOIST bit 2 (FQ): the next level's v[p] load is issued after this level's xy sums
+    {12, 5, 2, 1, 8, 1, 1, 0, 1, 1, 1, 4, 0, 1, 2, 1},  // 128: 123
+    {16, 4, 2, 1, 8, 1, 1, 0, 1, 1, 1, 4, 0, 1, 2, 1},  // 129: 117
+    {12, 5, 2, 1, 8, 1, 1, 0, 1, 1, 1, 5, 0, 1, 2, 1},  // 130: 123, and level 1's sums before the TMA wait
+    {12, 5, 2, 1, 8, 1, 1, 0, 1, 1, 1, 1, 0, 1, 2, 1},  // 131: 123, level 1's sums before the TMA wait
 };
-constexpr int kNumVariants = 128;
+constexpr int kNumVariants = 132;
 static_assert(sizeof(kVariants) / sizeof(Variant) == kNumVariants, "variant table size");
 // Variants compiled per (dtype, T): keeps build time bounded.  Variant 0
 // (16x2, 2 slots) fits every depth and is the fallback.
@@ -252,9 +257,11 @@ constexpr bool compiled() {
     if (V == 80 || V == 92) return sizeof(R) == 4 && T >= 2;          // fp32 12x4, 12x6
     if (V == 96) return sizeof(R) == 4 && T >= 2 && T <= 6;           // fp32 12x6 hoisted
     if (V >= 75 && V <= 109) return false;
-    if (V >= 110 && V <= 117) return T >= 2;
-    if (V == 118 || V == 119) return sizeof(R) == 4 && T >= 2;
-    if (V >= 120 && V <= 127) return T >= 2;
+    // FQ shapes still built (defaults and their closest rivals)
+    if (V == 110 || V == 111 || V == 112 || V == 117 || V == 121 || V == 126) return T >= 2;
+    if (V == 123 || V == 130) return sizeof(R) == 8 && T >= 2 && T <= 4;
+    if (V == 125) return sizeof(R) == 4 && T >= 2;                    // fp32 12x6, early level-1 sums
+    if (V >= 110 && V <= 131) return false;
 
     if (V == 8) return sizeof(R) == 4 && T >= 3 && T <= 4;
     if (V == 9 || V == 10) return T <= 4;
@@ -289,7 +296,8 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
         return fail(SP_ERR_SCHEDULE, "kernel variant %d not built for depth %d", V, T);
     } else {
         constexpr Variant v = kVariants[V];
-        static_assert((v.lag == 1 && !v.tq) || (!PEER && !INPL), "lag-2 / tensor-memory variants: two-grid passes only");
+        static_assert(v.lag == 1 || (!PEER && !INPL), "lag-2 variants: two-grid passes only");
+        static_assert(!v.tq || !PEER, "tensor-memory variants: no peer stores");
         constexpr bool two_arg = v.lag == 2 || v.tq;   // kernels without the saved-rows tensor map
         using Pl = std::conditional_t<
             v.tq != 0, sp::PlanQ<R, T, v.by, v.py, v.ring, v.fq>,
@@ -297,7 +305,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
                                sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls, v.ys>>>;
         auto kern = [] {
             constexpr Variant w = kVariants[V];
-            if constexpr (w.tq) return sp::tq_kernel<R, T, w.by, w.py, w.ring, w.hoist, w.sg, w.fq>;
+            if constexpr (w.tq) return sp::tq_kernel<R, T, w.by, w.py, w.ring, w.hoist, w.sg, w.fq, INPL>;
             else if constexpr (w.lag == 2) return sp::tb2_kernel<R, T, w.by, w.py, w.minb, w.ring>;
             else return sp::tb_kernel<R, T, w.by, w.py, w.slots, w.minb, w.ring, w.rstore, w.split, PEER, w.cl,
                                       w.ls, INPL, w.hoist, w.ys>;
@@ -511,7 +519,11 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
         case 124: return launch_tb_t<R, T, 124>(src, L, a, grid, s);
         case 125: return launch_tb_t<R, T, 125>(src, L, a, grid, s);
         case 126: return launch_tb_t<R, T, 126>(src, L, a, grid, s);
-        default: return launch_tb_t<R, T, 127>(src, L, a, grid, s);
+        case 127: return launch_tb_t<R, T, 127>(src, L, a, grid, s);
+        case 128: return launch_tb_t<R, T, 128>(src, L, a, grid, s);
+        case 129: return launch_tb_t<R, T, 129>(src, L, a, grid, s);
+        case 130: return launch_tb_t<R, T, 130>(src, L, a, grid, s);
+        default: return launch_tb_t<R, T, 131>(src, L, a, grid, s);
     }
 }
 
@@ -526,17 +538,19 @@ constexpr int kPeerVariant = 0;
 // T=3 12x3, T=4 8x4/3, fp32 T=2) would spill.  fp64 T=2,3: 8x4/3 with one
 // __syncthreads per step (measured: 562 / 524-538 GLUP/s against 457 / 512
 // for 16x2/3 and 8x4/2 with the split barrier; at T=4 it spills: 355 vs 507).
+// Since the tensor-memory kernels (tq_kernel) the deeper in-place passes run on their FQ
+// forms, whose step body is not register-critical (the hooks cost nothing there).
 #ifndef SP_INPL64_T2
 #define SP_INPL64_T2 13
 #endif
 #ifndef SP_INPL64_T3
-#define SP_INPL64_T3 34   // 12x3/2 hoisted: 603 / 620 GLUP/s at chunk 64 / 128 (13: 550 / 595)
+#define SP_INPL64_T3 111  // FQ 8x8 (round 2, 12x3/2 hoisted: 603 / 620 GLUP/s at chunk 64 / 128)
 #endif
 #ifndef SP_INPL64_T4
-#define SP_INPL64_T4 12
+#define SP_INPL64_T4 123  // FQ 12x5 (round 2, 8x4/2: 512)
 #endif
-constexpr int kInplaceF64[9] = {0, 5, SP_INPL64_T2, SP_INPL64_T3, SP_INPL64_T4, 12, 12, 12, 12};
-constexpr int kInplaceF32[9] = {0, 14, 4, 22, 8, 11, 11, 2, 2};
+constexpr int kInplaceF64[9] = {0, 5, SP_INPL64_T2, SP_INPL64_T3, SP_INPL64_T4, 110, 112, 112, 112};
+constexpr int kInplaceF32[9] = {0, 14, 4, 22, 92, 92, 121, 121, 111};
 
 template <typename R, int T>
 constexpr int inplace_variant() {

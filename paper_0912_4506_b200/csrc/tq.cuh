@@ -152,7 +152,9 @@ struct PlanQ {
 
 // HOIST bit 0: level 1's xy sums before the TMA wait; bit 1: the deeper levels'
 // right after the step barrier (independent chains ahead of the level loop)
-template <typename R, int T, int BY, int PY, int RCAP, int HOIST, int SG = 0, int FQ = 0>
+// INPL: in-place pass of compressed storage (tb_kernel's hooks: chunk order, z shift of the
+// stores, per-chunk completion counters; TBArgs::cdone)
+template <typename R, int T, int BY, int PY, int RCAP, int HOIST, int SG = 0, int FQ = 0, bool INPL = false>
 __global__ void __launch_bounds__(32 * BY, 1)
     tq_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     using A = Arith<R>;
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
         }
         uid[pseq++ & (P::NUID - 1)] = pu < a.units ? pu : -1;
         if (pu >= a.units) return;
-        const Unit pw = decode_unit(a, pu);
+        const Unit pw = decode_unit<INPL>(a, pu);
         pc0 = footprint_x<R>(a, pw.x0, T) + a.x_off;
         pc1 = pw.y0 - T + a.gy;
         pc2 = pw.zc0 - T + a.gz;
@@ -230,6 +232,9 @@ __global__ void __launch_bounds__(32 * BY, 1)
         producer_unit();
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
         for (int i = 0; i < RING_N - 1; ++i) produce(i);
+    }
+    if constexpr (INPL) {   // the first unit's dependencies (see the end of the unit loop)
+        if (threadIdx.x == 0 && uid[0] >= 0) wait_chunks_read(a, decode_unit<INPL>(a, uid[0]).c);
     }
     __syncwarp();
 
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
         mbar_wait(&full[gstep % RING_N], (gstep / RING_N) & 1);
         const int u = uid[cseq & (P::NUID - 1)];
         if (u < 0) break;
-        const Unit w = decode_unit(a, u);
+        const Unit w = decode_unit<INPL>(a, u);
         const int fx = footprint_x<R>(a, w.x0, T), fy = w.y0 - T;
         const int nsteps = (w.zc1 - w.zc0) + 2 * T;
 
@@ -302,7 +307,8 @@ __global__ void __launch_bounds__(32 * BY, 1)
         }
         R* dcol = reinterpret_cast<R*>(a.dst) + a.origin + (int64_t)(fy + cy) * a.py + (fx + cx);
         const int64_t pz = a.pz, py = a.py;
-        R* dnext = dcol + (int64_t)(w.zc0 - 2 * T) * pz;   // plane q-T of step 0
+        // plane q-T of step 0 (INPL: level-T plane p goes to plane p + zshift)
+        R* dnext = dcol + (int64_t)(w.zc0 - 2 * T + (INPL ? a.zshift : 0)) * pz;
         const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
         const bool full_rows = vec_store && wyb == (1u << PY) - 1u;
 
@@ -494,6 +500,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
         // carries a value from one step to the next.
         auto stepf = [&](auto fast, int st) __attribute__((always_inline)) {
             constexpr bool FAST = decltype(fast)::value;
+            constexpr bool LATEC = FAST && (HOIST & 4);   // HOIST bit 2: see the loads below
             const int slot = gstep % RING_N;
             const int pslot = (gstep + RING_N - 1) % RING_N;
             const int pslot2 = (gstep + RING_N - 2) % RING_N;
@@ -594,11 +601,17 @@ __global__ void __launch_bounds__(32 * BY, 1)
                                 TP::get(rm + (j * PX + 1) * TP::W), nn[j][0], nn[j][1]);
                     }
                 }
-                if (t < T) {
-                    tm_ld<NR>(tm + t * 2 * NR + sm, rm);
-                    tm_ld<NR>(tm + t * 2 * NR + sc, rc);
+                // next level's v[p-1] now (rm is consumed); its v[p] once the xy sums have
+                // consumed this level's (LDTM wants one block of registers: loading it while
+                // cc is live costs a copy per register)
+                if (t < T) tm_ld<NR>(tm + t * 2 * NR + sm, rm);
+                if constexpr (!LATEC) {
+                    if (t < T) tm_ld<NR>(tm + t * 2 * NR + sc, rc);
                 }
                 if (!early) xy();
+                if constexpr (LATEC) {
+                    if (t < T) tm_ld<NR>(tm + t * 2 * NR + sc, rc);
+                }
                 uint32_t inm = 0;
                 if constexpr (!FAST) {
                     const int p = q - t;
@@ -704,6 +717,19 @@ __global__ void __launch_bounds__(32 * BY, 1)
                 for (int j = 0; j < PY; ++j)
 #pragma unroll
                     for (int i = 0; i < PX; ++i) C[0][t][j][i] = C[1][t][j][i];
+        }
+        if constexpr (INPL) {
+            if (threadIdx.x == 0) {
+                // this thread consumed the unit's last plane: all its global reads (TMA) are done.
+                // The next unit stores over planes chunks c-2, c-3 read: wait for them here; the
+                // other warps store only after a step barrier has seen this thread's next arrival.
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __threadfence();
+                atomicAdd(a.cdone + w.c, 1u);
+                const int nu = uid[(cseq + 1) & (P::NUID - 1)];
+                if (nu >= 0) wait_chunks_read(a, decode_unit<INPL>(a, nu).c);
+            }
+            __syncwarp();
         }
     }
     tm_wait_st();

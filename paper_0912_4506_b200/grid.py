@@ -408,7 +408,16 @@ class CompressedGrid:
             self._shell = torch.empty(nshell, dtype=self.torch_dtype, device=self.device)
             nch = -(-dims.nz // self.chunk)
             self._counters = torch.zeros(nch, dtype=torch.int32, device=self.device)
+        self._offset0 = offset0
         self._fill(pattern)
+        self._gather_shell()
+
+    def reset(self, pattern=None) -> None:
+        """Re-initialise the box from ``pattern`` (default: the construction pattern) at
+        its starting offset, as constructing the grid again would."""
+        self.offset = self._offset0
+        self._ascend_next = True
+        self._fill(self.pattern if pattern is None else pattern)
         self._gather_shell()
 
     # -- storage -------------------------------------------------------------

@@ -19,13 +19,12 @@ from . import _native as N
 from .grid import GridDims, TwoGrid, _on
 
 # Levels fused per HBM pass when the config does not say: the depth with the
-# highest SUSTAINED throughput on B200 (C3 1024^3 fp64, 100 sweeps: T=2 646,
-# T=3 723, T=4 757 GLUP/s -- T=2 saturates HBM and runs into the board power
-# cap at ~1640 MHz, T=4 stays near 1900 MHz).
+# highest SUSTAINED throughput on B200 (C3 1024^3 fp64, 100 sweeps, tensor-memory
+# kernels: T=3 744, T=4 840, T=5 821 GLUP/s -- T <= 3 saturates HBM and runs into the
+# board power cap at ~1700 MHz).
 DEFAULT_DEPTH = {N.SP_F64: 4, N.SP_F32: 4}
-# In-place passes (compressed storage) run fastest at T=3 (C3 1024^3, chunk 64: T=2 566, T=3 603,
-# T=4 517 GLUP/s; the per-unit chunk wait makes deeper in-place passes spill).
-DEFAULT_DEPTH_INPLACE = {N.SP_F64: 3, N.SP_F32: 4}
+# In-place passes (compressed storage), C3 1024^3 at chunk 64: T=3 662, T=4 791, T=5 728 GLUP/s.
+DEFAULT_DEPTH_INPLACE = {N.SP_F64: 4, N.SP_F32: 4}
 MAX_DEPTH = 8
 
 

@@ -299,7 +299,7 @@ def test_c1_full_grid_vs_reference(sp, kat, ref_fields):
     assert bitwise(inner[kat["c1_planes_index"]], ref_fields["c1_planes_l100"])
 
 
-@pytest.mark.parametrize("shape_id", list(range(1, 129)))
+@pytest.mark.parametrize("shape_id", list(range(1, 133)))
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_every_cta_shape(sp, O, shape_id, dtype):
     lib = sp._native.lib()
