@@ -518,8 +518,15 @@ def main():
                         "algorithmic_bytes_per_lup": round(2 * es / T, 3),
                         "fp64_pipe_active_pct": tj[key].get("fp64_pipe_active_pct"),
                         "issue_active_pct": tj[key].get("issue_active_pct"),
+                        "lsu_pipe_pct": tj[key].get("lsu_pipe_pct"),
                         "source": tj[key].get("source")}
 
+    # the K2 kernel of this depth: tq_kernel (z-queue in tensor memory) or tb_kernel (register queue)
+    k2_desc = N.describe_variant(sp_dtype, T) if cuda else ""
+    if args.storage == "twogrid":
+        k2_name = "tq_kernel" if "tensor memory" in k2_desc else "tb_kernel"
+    else:   # in-place passes: the FQ forms of tq_kernel from T=3 (csrc/host.cuh, kInplace*)
+        k2_name = "tq_kernel (in place)" if T >= (3 if dt == "f64" else 4) else "tb_kernel (in place)"
     R_hbm = hbm * T / (2 * es)                      # GLUP/s, HBM term
     R_fp = p_fp64 / 6 / 1e9 if dt == "f64" and cuda else float("inf")
     R = min(R_hbm, R_fp) * world
@@ -581,7 +588,7 @@ def main():
                        "hbm_grid_bytes": sum(b.numel() * b.element_size() for b in grid.buffers)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": traffic,
-                         "kernel": f"tb_kernel T={T}", "peak_source": hbm_src,
+                         "kernel": "%s T=%d" % (k2_name, T), "peak_source": hbm_src,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": round(t_pass * 1e3, 3), "ncu": ncu_evidence},
             "temporal_roofline": {"T": T, "R_glups": round(R, 1), "frac": round(value / R, 4),
