@@ -198,7 +198,14 @@ __global__ void __launch_bounds__(32 * BY, 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // this thread's TMEM lane and first column: M[l] at tm + l * NR
+    // (read through lane 0: the compiler then knows the address is warp-uniform and keeps it in a
+    // uniform register instead of converting it before every tcgen05.ld/st)
+#ifndef SP_TM_NOUNIFORM
+    const uint32_t tm = __shfl_sync(0xffffffffu,
+                                    *tbase + ((uint32_t)(32 * (wy & 3)) << 16) + (uint32_t)((wy >> 2) * P::GCOLS), 0);
+#else   // A/B builds
     const uint32_t tm = *tbase + ((uint32_t)(32 * (wy & 3)) << 16) + (uint32_t)((wy >> 2) * P::GCOLS);
+#endif
 
     // producer (thread 0): as in tb_kernel
     int pu = -1, pseq = 0, pc0 = 0, pc1 = 0, pc2 = 0, pc2_end = 0;
