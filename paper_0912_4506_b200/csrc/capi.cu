@@ -897,7 +897,7 @@ int sweep_part(const void* src, void* dst, int dtype, const sp_layout* L, int T,
         if ((nxo + ox_pair - 1) / ox_pair == (nxo + a.ox - 1) / a.ox) a.ox = ox_pair;
     }
     const int64_t out_cells = (out_hi[0] - out_lo[0]) * (out_hi[1] - out_lo[1]) * (out_hi[2] - out_lo[2]);
-    const int variant = peer ? kPeerVariant
+    const int variant = peer ? (dtype == SP_F64 ? kPeerF64 : kPeerF32)[T]
                              : (inplace ? inplace_variant_rt(dtype, T) : variant_for(dtype, T, out_cells));
     const int cl = kVariants[variant].cl;
     const int wy = kVariants[variant].by * kVariants[variant].py * cl;   // cluster footprint rows

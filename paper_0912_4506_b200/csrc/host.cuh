@@ -297,7 +297,6 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
     } else {
         constexpr Variant v = kVariants[V];
         static_assert(v.lag == 1 || (!PEER && !INPL), "lag-2 variants: two-grid passes only");
-        static_assert(!v.tq || !PEER, "tensor-memory variants: no peer stores");
         constexpr bool two_arg = v.lag == 2 || v.tq;   // kernels without the saved-rows tensor map
         using Pl = std::conditional_t<
             v.tq != 0, sp::PlanQ<R, T, v.by, v.py, v.ring, v.fq>,
@@ -305,7 +304,7 @@ int launch_tb_t(const void* src, const sp_layout* L, const sp::TBArgs& a, int gr
                                sp::Plan<R, T / v.ls, v.by, v.py, v.slots, v.minb, v.ring, v.cl, v.ls, v.ys>>>;
         auto kern = [] {
             constexpr Variant w = kVariants[V];
-            if constexpr (w.tq) return sp::tq_kernel<R, T, w.by, w.py, w.ring, w.hoist, w.sg, w.fq, INPL>;
+            if constexpr (w.tq) return sp::tq_kernel<R, T, w.by, w.py, w.ring, w.hoist, w.sg, w.fq, INPL, PEER>;
             else if constexpr (w.lag == 2) return sp::tb2_kernel<R, T, w.by, w.py, w.minb, w.ring>;
             else return sp::tb_kernel<R, T, w.by, w.py, w.slots, w.minb, w.ring, w.rstore, w.split, PEER, w.cl,
                                       w.ls, INPL, w.hoist, w.ys>;
@@ -527,9 +526,16 @@ int launch_variant(int v, const void* src, const sp_layout* L, const sp::TBArgs&
     }
 }
 
-// Peer-store launches (boundary slabs of a z-slab rank) use the fallback
-// variant 0 only: they cover h planes, a small share of a step.
-constexpr int kPeerVariant = 0;
+// Peer-store launches (boundary slabs of a z-slab rank: h planes each, stored a second time
+// into the z neighbours' ghost planes) run the depth's default kernel where that is a
+// tensor-memory kernel, the fallback tb_kernel variant 0 otherwise.
+constexpr int kPeerF64[9] = {0, 0, 0, 89, 130, 110, 112, 112, 112};
+constexpr int kPeerF32[9] = {0, 0, 0, 0, 92, 92, 121, 121, 111};
+template <typename R, int T>
+constexpr int peer_variant() {
+    if constexpr (sizeof(R) == 8) return kPeerF64[T];
+    else return kPeerF32[T];
+}
 
 // In-place passes (compressed storage) are separate instantiations with the
 // in-place hooks (keeping their registers out of the two-grid kernels).  The
@@ -563,7 +569,7 @@ constexpr int inplace_variant() {
 template <typename R, int T>
 int launch_kind(int kind, int v, const void* src, const sp_layout* L, const sp::TBArgs& a, int grid,
                 cudaStream_t s) {
-    if (kind == 1) return launch_tb_t<R, T, kPeerVariant, true>(src, L, a, grid, s);
+    if (kind == 1) return launch_tb_t<R, T, peer_variant<R, T>(), true>(src, L, a, grid, s);
     if (kind == 2) return launch_tb_t<R, T, inplace_variant<R, T>(), false, true>(src, L, a, grid, s);
     return launch_variant<R, T>(v, src, L, a, grid, s);
 }

@@ -24,7 +24,7 @@
 //
 // Wavefront, arithmetic, summation order and the Dirichlet/domain rule are
 // tb_kernel's (level t trails level t-1 by one plane; bit-identical results).
-// Plain two-grid passes only (no peer stores, in-place passes or clusters).
+// No cluster forms; in-place (INPL) and peer-store (PEER) passes as tb_kernel.
 // (R/pipeline.py:395-408 is the reference's per-block level loop.)
 
 #define SP_TM_R4(r, o) "=r"(r[o]), "=r"(r[o + 1]), "=r"(r[o + 2]), "=r"(r[o + 3])
@@ -153,8 +153,10 @@ struct PlanQ {
 // HOIST bit 0: level 1's xy sums before the TMA wait; bit 1: the deeper levels'
 // right after the step barrier (independent chains ahead of the level loop)
 // INPL: in-place pass of compressed storage (tb_kernel's hooks: chunk order, z shift of the
-// stores, per-chunk completion counters; TBArgs::cdone)
-template <typename R, int T, int BY, int PY, int RCAP, int HOIST, int SG = 0, int FQ = 0, bool INPL = false>
+// stores, per-chunk completion counters; TBArgs::cdone).  PEER: boundary-slab pass of a z-slab
+// rank that also stores its planes into the neighbours' ghost planes.
+template <typename R, int T, int BY, int PY, int RCAP, int HOIST, int SG = 0, int FQ = 0, bool INPL = false,
+          bool PEER = false>
 __global__ void __launch_bounds__(32 * BY, 1)
     tq_kernel(const __grid_constant__ CUtensorMap tmap, const TBArgs a) {
     using A = Arith<R>;
@@ -319,6 +321,33 @@ __global__ void __launch_bounds__(32 * BY, 1)
         const bool vec_store = wx == 3u && ((reinterpret_cast<uintptr_t>(dcol) & (sizeof(V2) - 1)) == 0);
         const bool full_rows = vec_store && wyb == (1u << PY) - 1u;
 
+        // level T: the finished plane p (16-byte streaming stores; lanes outside the tile's
+        // columns skip the block).  PEER: planes of the slab's halo depth also go into the z
+        // neighbours' ghost planes (peer memory; TBArgs::rd_lo/rd_hi, as tb_kernel)
+        auto store_plane = [&](const R(&out)[PY][PX], int p) __attribute__((always_inline)) {
+            auto put = [&](R* b) __attribute__((always_inline)) {
+                if (full_rows) {
+#pragma unroll
+                    for (int j = 0; j < PY; ++j) __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
+                } else if (vec_store) {
+#pragma unroll
+                    for (int j = 0; j < PY; ++j)
+                        if ((wyb >> j) & 1u) __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
+                } else if (wx != 0u) {
+#pragma unroll
+                    for (int j = 0; j < PY; ++j) {
+                        const bool row = (wyb >> j) & 1u;
+                        if (row && (wx & 1u)) __stcs(b + j * py, out[j][0]);
+                        if (row && (wx & 2u)) __stcs(b + j * py + 1, out[j][1]);
+                    }
+                }
+            };
+            put(dnext);
+            if constexpr (PEER) {
+                if (p < a.rz_lo) put(dnext + a.rd_lo);
+                if (p >= a.rz_hi) put(dnext + a.rd_hi);
+            }
+        };
         auto step = [&](auto phase, auto fast, int st) __attribute__((always_inline)) {
             constexpr int PH = decltype(phase)::value;
             constexpr bool FAST = decltype(fast)::value;
@@ -468,24 +497,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
                     *reinterpret_cast<V2*>(E + (2 * wy + 1) * WX + cx) = V2{dst[PY - 1][0], dst[PY - 1][1]};
                 }
             }
-            if (st >= 2 * T) {
-                R* b = dnext;
-                if (full_rows) {
-#pragma unroll
-                    for (int j = 0; j < PY; ++j) __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
-                } else if (vec_store) {
-#pragma unroll
-                    for (int j = 0; j < PY; ++j)
-                        if ((wyb >> j) & 1u) __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
-                } else if (wx != 0u) {
-#pragma unroll
-                    for (int j = 0; j < PY; ++j) {
-                        const bool row = (wyb >> j) & 1u;
-                        if (row && (wx & 1u)) __stcs(b + j * py, out[j][0]);
-                        if (row && (wx & 2u)) __stcs(b + j * py + 1, out[j][1]);
-                    }
-                }
-            }
+            if (st >= 2 * T) store_plane(out, q - T);
             dnext += pz;
             __syncwarp();
             if constexpr (T >= 2) {
@@ -663,24 +675,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
                 }
             }
             const R(&out)[PY][PX] = lv[T];
-            if (st >= 2 * T) {
-                R* b = dnext;
-                if (full_rows) {
-#pragma unroll
-                    for (int j = 0; j < PY; ++j) __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
-                } else if (vec_store) {
-#pragma unroll
-                    for (int j = 0; j < PY; ++j)
-                        if ((wyb >> j) & 1u) __stcs(reinterpret_cast<V2*>(b + j * py), V2{out[j][0], out[j][1]});
-                } else if (wx != 0u) {
-#pragma unroll
-                    for (int j = 0; j < PY; ++j) {
-                        const bool row = (wyb >> j) & 1u;
-                        if (row && (wx & 1u)) __stcs(b + j * py, out[j][0]);
-                        if (row && (wx & 2u)) __stcs(b + j * py + 1, out[j][1]);
-                    }
-                }
-            }
+            if (st >= 2 * T) store_plane(out, q - T);
             dnext += pz;
             __syncwarp();
             if (lane == 0) mbar_arrive(&lbar[gstep & 1u]);

@@ -38,6 +38,7 @@ def _bitwise(a, b):
     (3, 4, [4, 3, 4], (41, 20, 130)),     # uneven split (14, 14, 13), remainder step
     (4, 1, [1] * 5, (17, 9, 33)),
     (2, 8, [8, 8], (50, 24, 24)),
+    (2, 7, [7, 6, 5], (44, 30, 66)),      # peer-store forms of the depth-5..7 kernels
 ])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_emulated_peer_slabs(sp, O, ranks, h, levels, shape, dtype):
