@@ -231,6 +231,38 @@ int sp_ghost_shell_region(void* base, int dtype, const sp_layout* L, const void*
  * Returns the variant index (>= 0) or a negative error code. */
 int sp_describe_variant(int dtype, int T, char* buf, int buflen);
 
+/* ---- z-slab multi-GPU behind the ABI (one process per GPU; NCCL bound at run
+ * time with dlopen("libnccl.so.2"), override with the environment variable
+ * SP_NCCL_LIB).  The overlapped and peer-store transports are driven by the
+ * Python SlabRunner; these entry points are the reference's strict
+ * alternation of exchange and compute for hosts without PyTorch. ------------- */
+#define SP_DIST_ID_BYTES 128
+typedef struct sp_dist sp_dist;
+
+/* Rank 0 creates the communicator id (ncclGetUniqueId); the host ships its
+ * SP_DIST_ID_BYTES bytes to every rank (the role of the reference's transport
+ * rendezvous, R/decomp.py:240-255). */
+int sp_dist_unique_id(void* id_out, int64_t len);
+
+/* Join the communicator as `rank` of `world` z-slab ranks on the current CUDA
+ * device (ranks are z-ordered: rank r's z- neighbour is r-1). */
+int sp_dist_create(const void* id, int rank, int world, sp_dist** out);
+int sp_dist_destroy(sp_dist* d);
+
+/* exchange_halos, z phase (R/decomp.py:149-179): the first / last h interior
+ * planes of `grid` go to the z- / z+ neighbour's ghost planes, and theirs come
+ * into this grid's ghost planes [-h, 0) and [nz, nz + h); whole padded planes,
+ * grouped ncclSend/ncclRecv on `stream`.  1 <= h <= L->gz. */
+int sp_dist_exchange_z(sp_dist* d, void* grid, int dtype, const sp_layout* L, int64_t h, void* stream);
+
+/* One outer step (R/decomp.py:208-237 after :149-179): exchange the depth-T
+ * halos of src, then T levels src -> dst on the rank's extended level domains
+ * (level_domains_for_rank, R/decomp.py:192-205: extended by T-t towards each
+ * neighbour, Dirichlet at physical walls) in one K2 pass.  The caller swaps
+ * src and dst afterwards (dst's ghosts are refreshed by the next step's
+ * exchange).  Requires L->gz >= T. */
+int sp_dist_step(sp_dist* d, void* src, void* dst, int dtype, const sp_layout* L, int T, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

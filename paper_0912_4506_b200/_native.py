@@ -19,7 +19,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 LIB_NAME = "libstencilpipe_b200.so"
 LIB_PATH = os.environ.get("SP_LIB_PATH") or os.path.join(_HERE, LIB_NAME)
-SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "jacobi_kernels.cuh", "host.cuh", "tb_inst.cu")]
+SOURCES = [os.path.join(_HERE, "csrc", f) for f in ("capi.cu", "jacobi_kernels.cuh", "host.cuh", "tb_inst.cu", "tq.cuh",
+                                                     "wave2.cuh", "dist_nccl.cu")]
 HEADER = os.path.join(_ROOT, "include", "stencilpipe_b200.h")
 
 SP_OK, SP_ERR_GRID, SP_ERR_SCHEDULE, SP_ERR_DECOMP, SP_ERR_DEVICE, SP_ERR_ARG = range(6)
@@ -37,7 +38,8 @@ EXPORTS = ("sp_version", "sp_last_error", "sp_launch_count", "sp_layout_make", "
            "sp_update_region", "sp_sweep_tb", "sp_sweep_tb_part", "sp_sweep_tb_part_peer", "sp_run_sweeps",
            "sp_digest", "sp_probe_fp64", "sp_set_tuning", "sp_set_schedule", "sp_ipc_export",
            "sp_ipc_import", "sp_ipc_close", "sp_copy_in", "sp_copy_out", "sp_describe_variant",
-           "sp_sweep_tb_inplace", "sp_ghost_shell", "sp_ghost_shell_elems", "sp_ghost_shell_region", "sp_copy_box")
+           "sp_sweep_tb_inplace", "sp_ghost_shell", "sp_ghost_shell_elems", "sp_ghost_shell_region", "sp_copy_box",
+           "sp_dist_unique_id", "sp_dist_create", "sp_dist_destroy", "sp_dist_exchange_z", "sp_dist_step")
 
 
 class NativeUnavailable(RuntimeError):
@@ -78,7 +80,8 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None,
     cflags = [f for f in NVCC_FLAGS if f != "--shared"]
     # one unit for the C ABI + small kernels, one per (dtype, T) for the K2
     # instantiations (host.cuh / tb_inst.cu): compiled in parallel
-    jobs = [("capi", [os.path.join(_HERE, "csrc", "capi.cu")])]
+    jobs = [("capi", [os.path.join(_HERE, "csrc", "capi.cu")]),
+            ("dist_nccl", [os.path.join(_HERE, "csrc", "dist_nccl.cu")])]
     for r in ("double", "float"):
         for t in range(1, 9):
             jobs.append((f"tb_{r}_{t}", [f"-DSP_INST_R={r}", f"-DSP_INST_T={t}",
@@ -93,7 +96,7 @@ def build(verbose: bool = False, force: bool = False, out: str | None = None,
     from concurrent.futures import ThreadPoolExecutor
     workers = max(1, min(len(jobs), (os.cpu_count() or 4)))
     # the heaviest units first (deep fp64 / fp32 instantiations)
-    order = sorted(jobs, key=lambda j: (j[0] == "capi", -int(j[0][-1]) if j[0] != "capi" else 0))
+    order = sorted(jobs, key=lambda j: (not j[0].startswith("tb_"), -int(j[0][-1]) if j[0].startswith("tb_") else 0))
     with ThreadPoolExecutor(workers) as ex:
         results = list(ex.map(compile_one, order))
     log = []
@@ -164,6 +167,12 @@ def load_library():
         L.sp_copy_box.argtypes = [vp, vp, ctypes.c_int] + [ctypes.c_int64] * 7 + [vp]
         L.sp_ghost_shell_elems.restype = ctypes.c_int64
         L.sp_ghost_shell_elems.argtypes = [ctypes.c_int64] * 3
+    if hasattr(L, "sp_dist_create") or not override:
+        L.sp_dist_unique_id.argtypes = [vp, ctypes.c_int64]
+        L.sp_dist_create.argtypes = [vp, ctypes.c_int, ctypes.c_int, P(vp)]
+        L.sp_dist_destroy.argtypes = [vp]
+        L.sp_dist_exchange_z.argtypes = [vp, vp, ctypes.c_int, P(Layout), ctypes.c_int64, vp]
+        L.sp_dist_step.argtypes = [vp, vp, vp, ctypes.c_int, P(Layout), ctypes.c_int, vp]
     if hasattr(L, "sp_describe_variant") or not override:
         L.sp_describe_variant.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_char_p, ctypes.c_int]
     for name in EXPORTS:
