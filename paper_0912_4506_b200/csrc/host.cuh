@@ -53,6 +53,10 @@ struct Variant {
     int sg = 0;                      // tq_kernel: columns per tcgen05.st (0: one wide store per level)
     int fq = 0;                      // tq_kernel: 1 = v[p] in tensor memory too (no z-queue registers)
 };
+// The table is append-only (profiles/*_tuning.md cite variants by index).  A note like
+// "fp64 T=4" on a row records the depth it was tuned for when it was added; the CURRENT
+// defaults are default_variant() in capi.cu (tq_kernel rows 75+ from T=3), the in-place and
+// peer-store picks are kInplace*/kPeer* below, and compiled<>() says which rows are still built.
 constexpr Variant kVariants[] = {
     {16, 2, 2, 1, 8, 0, 0},  // 0: fallback for every depth
     {16, 2, 3, 1, 8, 0, 1},  // 1: fp64 T=3
