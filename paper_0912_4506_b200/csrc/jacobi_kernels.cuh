@@ -115,12 +115,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t addr = smem_u32(bar);
     uint32_t ok = 0;
     do {
+        // the suspend-time hint (ns) lets a waiting thread sleep in the barrier unit instead of
+        // returning to spin: fewer TRYWAIT/BRA issues next to the working warps (fp32 T=4 +3 %,
+        // fp64 T=3..4 +1 %, same-box A/B)
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(ok)
-            : "r"(addr), "r"(parity)
+            : "r"(addr), "r"(parity), "r"(4000u)
             : "memory");
     } while (!ok);
 }
