@@ -205,3 +205,18 @@ def test_cuda_engine_default_depth():
     assert CudaEngine().default_depth(G()) == DEFAULT_DEPTH[N.SP_F64]
     G.sp_dtype = N.SP_F32
     assert CudaEngine().default_depth(G()) == DEFAULT_DEPTH[N.SP_F32]
+
+
+def test_k2_sass_uses_tma_and_tensor_memory_and_no_fma():
+    """The fp64 T=4 K2 unit as built: TMA loads, tensor-memory ld/st (tq_kernel's z-queue) and
+    not one DFMA (bit-exactness with the reference's add/multiply order forbids contraction).
+    Reads the object the build left in-tree; skips where it or cuobjdump is absent."""
+    import shutil
+    import subprocess
+    obj = os.path.join(ROOT, "paper_0912_4506_b200", "build", "obj", "tb_double_4.o")
+    if not os.path.exists(obj) or not shutil.which("cuobjdump"):
+        pytest.skip("no build objects / cuobjdump here")
+    sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True, check=True).stdout
+    count = {m: len(re.findall(r"\b%s\b" % m, sass)) for m in ("UTMALDG", "LDTM", "STTM", "DADD", "DMUL", "DFMA")}
+    assert count["UTMALDG"] > 0 and count["LDTM"] > 0 and count["STTM"] > 0, count
+    assert count["DADD"] > 0 and count["DMUL"] > 0 and count["DFMA"] == 0, count
