@@ -150,8 +150,10 @@ struct PlanQ {
                                    NUID * 4 + 16;
 };
 
-// HOIST bit 0: level 1's xy sums before the TMA wait; bit 1: the deeper levels'
-// right after the step barrier (independent chains ahead of the level loop)
+// HOIST bit 0: level 1's xy sums before the TMA wait; bit 1 (tq form): the deeper levels'
+// right after the step barrier (independent chains ahead of the level loop); bit 2 (FQ form,
+// FAST steps): the next level's v[p] load is issued after this level's xy sums.
+// SG: columns per tcgen05.st (0 = one wide store per level).  FQ: see PlanQ.
 // INPL: in-place pass of compressed storage (tb_kernel's hooks: chunk order, z shift of the
 // stores, per-chunk completion counters; TBArgs::cdone).  PEER: boundary-slab pass of a z-slab
 // rank that also stores its planes into the neighbours' ghost planes.
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
                         else dst[j][i] = ((inm >> (j * PX + i)) & 1u) ? ups[i] : cc[j][i];
                     }
                 }
-                if (T >= 2 && t == 1 && gstep > 0) {
+                if (t == 1 && gstep > 0) {
                     // step k-1 is complete in every warp: its edge rows are visible, its
                     // reads of buffer `cur` and of ring plane q-2 are done
                     const uint32_t k1 = gstep - 1;
@@ -500,16 +502,7 @@ __global__ void __launch_bounds__(32 * BY, 1)
             if (st >= 2 * T) store_plane(out, q - T);
             dnext += pz;
             __syncwarp();
-            if constexpr (T >= 2) {
-                if (lane == 0) mbar_arrive(&lbar[gstep & 1u]);
-            } else {
-                // T = 1: no level planes; the ring slot of plane q-1 is free once every warp is here
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    produce(pslot);
-                }
-            }
+            if (lane == 0) mbar_arrive(&lbar[gstep & 1u]);
             __syncwarp();
             ++gstep;
         };
