@@ -675,7 +675,11 @@ __global__ void __launch_bounds__(32 * BY, 1)
             __syncwarp();
             ++gstep;
         };
+#ifndef SP_TQ_FORCE_SLOW
         const bool fast_xy = fastm == (1u << T) - 1u;
+#else   // diagnostic builds: every step takes the SLOW (per-cell select) path
+        const bool fast_xy = false;
+#endif
         using I0 = std::integral_constant<int, 0>;
         using I1 = std::integral_constant<int, 1>;
         // Steps run in pairs (parities 0, 1), so only C[0] is live between pairs; a

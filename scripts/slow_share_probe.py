@@ -43,3 +43,9 @@ for rep in range(2):
     # 16 x 17 whole tiles of the FQ 12x5 kernel (56 x 52 outputs), away from every x/y wall
     print("interior tiles     %.1f GLUP/s" % timed((0, 70, 64), (n, 70 + 17 * 52, 64 + 16 * 56)))
     print("x walls included   %.1f GLUP/s" % timed((0, 70, 0), (n, 70 + 17 * 52, n)))
+    # four tile columns each: at the left wall, in the middle, at the right wall (all full-width tiles)
+    for name, x0 in (("left wall", 0), ("middle", 448), ("right wall", n - 224)):
+        print("4 columns, %-10s %.1f GLUP/s" % (name, timed((0, 70, x0), (n, 70 + 17 * 52, x0 + 224))))
+    # four tile rows each (y): at the low wall, in the middle
+    for name, y0 in (("low wall", 0), ("middle", 416)):
+        print("4 rows, %-10s    %.1f GLUP/s" % (name, timed((0, y0, 64), (n, y0 + 208, 64 + 16 * 56))))
